@@ -1,0 +1,58 @@
+// Runner kernel launchers (generic families + utilities).  See kernels.cu and
+// tc_gemm.cu.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "plan.hpp"
+
+namespace lsb {
+
+// Strides (elements) of the three contraction operands per role.
+struct Strides {
+  int64_t sx[4], sy[4], sc[4];
+  int64_t ext[4];  // batch, m, n, k
+};
+
+// Reference output in float64 (one thread per output element).
+void launch_reference(const void* x, const void* y, double* out, const Strides& s, bool bf16, cudaStream_t st);
+// NAIVE family: one thread per output, fp32 accumulate.
+void launch_naive(const void* x, const void* y, float* c, const Strides& s, bool bf16, cudaStream_t st);
+// SIMT family (register-tile lattice).
+bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const SimtCfg& cfg, bool bf16,
+                 const unsigned long long* deadline, int* timed_out, cudaStream_t st);
+// LOOPNEST family.
+void launch_loopnest(const void* x, const void* y, float* c, const LoopNestCfg& cfg, bool bf16,
+                     const unsigned long long* deadline, int* timed_out, cudaStream_t st);
+// K6 parity reducer: slot[0] = max |c - ref| (as double bits), slot[1] = mismatches.
+void launch_parity(const float* c, const double* ref, int64_t n, double rtol, double atol,
+                   unsigned long long* slot, cudaStream_t st);
+// deadline = globaltimer + ns (device side, right before the guarded launch)
+void launch_set_deadline(unsigned long long* deadline, unsigned long long ns, cudaStream_t st);
+// spin on the device for ~ns (lets the host queue a chunk of launches)
+void launch_delay(unsigned long long ns, cudaStream_t st);
+// fp32 -> bf16 copy, and an optional 2-D transpose to make K contiguous
+void launch_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st);
+void launch_transpose_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t batch, int64_t rows,
+                           int64_t cols, cudaStream_t st);
+
+// Raise a kernel's dynamic smem limit to the device opt-in minus its static
+// smem; returns that limit or -1.
+int opt_in_dynamic_smem(const void* fn);
+
+// TCGEN05 family (tc_gemm.cu): tensor maps are built by the caller.
+struct TcLaunch {
+  const void* tmap_a;  // CUtensorMap* (host memory, passed by value to the kernel)
+  const void* tmap_b;
+  float* c;
+  int64_t sc_b, sc_m;  // output strides (elements) for batch and M (N contiguous)
+  int m, n, k;
+  int bn, splits, kt, stages, batch, grid_m, grid_n;
+  int accumulate;      // 1: split-K atomic accumulation into a zeroed C
+  int smem_bytes;
+};
+bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st);
+
+}  // namespace lsb

@@ -1,0 +1,103 @@
+// Trace-to-kernel instantiator: maps a final program (the replayed trace's
+// TensorProgram) to one kernel family + configuration.  It is a pure function
+// of the program (SURVEY.md §7 decision 3): search dedups by structural hash,
+// so every kernel knob must be visible in the loop nest.
+//
+// Mapping convention (replaces the absent `bind`, SURVEY.md §7 decision 4):
+//   * every loop of the contraction block is a part of one role axis
+//     (batch / M / N / K), recovered from the affine index expressions;
+//     adjacent parts of one axis are merged (same iteration order);
+//   * any non-serial loop kind            -> LOOPNEST: the parallel loop is the
+//     thread index, every other loop runs in order inside the thread;
+//   * one part per axis (the unscheduled e0) -> NAIVE: one thread per output;
+//   * innermost parts [M 128][N 16..256][K 64] with bf16 data -> TCGEN05:
+//     one UMMA tile per CTA, K parts hoisted above every spatial loop become
+//     split-K, the other outer K parts the k-tile pipeline, spatial parts the
+//     grid;
+//   * otherwise                            -> SIMT: spatial part 0 -> grid,
+//     part 1 -> threads, parts >= 2 -> per-thread register tile; innermost K
+//     part -> shared-memory k-tile (BK), outer K parts -> k-tile loop.
+// Configurations outside hardware limits are ILLEGAL (the paper's validator
+// for "beyond the physical hardware limit").
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ir.hpp"
+
+namespace lsb {
+
+enum Role { R_BATCH = 0, R_M = 1, R_N = 2, R_K = 3, R_COUNT = 4 };
+
+// The contraction C[b,m,n] += X[b,m,k] * Y[b,n,k] (any index order/layout)
+// recovered from e0.
+struct Workload {
+  std::string block;               // contraction block name
+  int x_buf = -1, y_buf = -1, c_buf = -1;
+  int64_t extent[R_COUNT] = {1, 1, 1, 1};
+  bool has_batch = false;
+  // element strides per role (0 when the role does not index the buffer)
+  int64_t sx[R_COUNT] = {0}, sy[R_COUNT] = {0}, sc[R_COUNT] = {0};
+  // witness (buffer, dim) whose index is exactly the role variable in e0
+  int wit_buf[R_COUNT] = {-1, -1, -1, -1}, wit_dim[R_COUNT] = {-1, -1, -1, -1};
+  std::vector<int> input_bufs;     // declared input order
+  int64_t x_elems = 0, y_elems = 0, c_elems = 0;
+  bool y_kmajor = false;           // K is Y's contiguous dim
+  bool x_kmajor = false;
+  double flops() const { return 2.0 * extent[0] * extent[1] * extent[2] * extent[3]; }
+};
+
+bool analyze_workload(const Program& e0, Workload* w, std::string* err);
+
+enum Family { F_NONE = 0, F_NAIVE = 1, F_SIMT = 2, F_TC = 3, F_LOOPNEST = 4 };
+enum PlanStatus { P_OK = 0, P_ILLEGAL = 1, P_UNSUPPORTED = 2, P_PARSE = 3 };
+
+struct Part { int role; int64_t extent; int64_t stride; Kind kind; };
+
+struct SimtCfg {
+  int64_t gb, gm, gn;     // grid
+  int64_t tb, tm, tn;     // threads
+  int64_t rb, rm, rn;     // per-thread tile (rb looped)
+  int64_t bk, kt;         // smem k-tile, k-tiles
+  int64_t smem_bytes;
+};
+
+struct TcCfg {
+  int64_t bn, splits, kt, grid_m, grid_n, batch;
+  int64_t stages, smem_bytes;
+};
+
+constexpr int kMaxLoopNest = 16;
+struct LoopNestCfg {
+  int n;
+  int64_t ext[kMaxLoopNest];
+  int64_t dx[kMaxLoopNest], dy[kMaxLoopNest], dc[kMaxLoopNest];
+};
+
+struct Plan {
+  int status = P_UNSUPPORTED;
+  int family = F_NONE;
+  std::string why;
+  std::vector<Part> parts;  // merged, nest order
+  SimtCfg simt{};
+  TcCfg tc{};
+  LoopNestCfg nest{};
+  bool needs_zero = false;  // output accumulated with += (memset first)
+  int32_t cfg[13] = {0};    // reporting
+};
+
+struct DeviceLimits {
+  int64_t max_threads = 1024;
+  int64_t max_smem = 227 * 1024;
+  bool bf16 = false;  // runner dtype
+};
+
+Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim);
+
+// Register-tile lattice compiled ahead of time for the SIMT family.
+bool simt_tile_supported(int64_t rm, int64_t rn);
+int simt_tile_index(int64_t v);  // index into {1,2,3,4,6,8,12,16} or -1
+
+}  // namespace lsb

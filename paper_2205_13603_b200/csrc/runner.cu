@@ -1,0 +1,581 @@
+// The B200 Runner: instantiate each candidate program as a kernel, run it,
+// check its output against the e0 reference output (K6) and time it with CUDA
+// events -- the hardware replacement of `_measure_batch`
+// (`src/search.py:249-256`) and of the baseline `simulate_latency(e0)`
+// (`src/search.py:326`).
+//
+// Timing protocol per ls_runner_measure call:
+//   phase A  (checked run)  for every launchable candidate: poison C with NaN,
+//            zero it when the family accumulates, arm a device-side deadline,
+//            launch once, run the parity reducer.  One sync for the batch.
+//   phase B  (timed run)    repeats sized from phase A (target_ms), launched
+//            back to back between two events per candidate.  Launches are
+//            queued in chunks behind a short device spin so the host has
+//            enqueued a whole chunk before its first event fires: the events
+//            bracket device execution, never host launch gaps.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/loopsched_b200.h"
+#include "common.hpp"
+#include "ir.hpp"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace lsb;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 K-major operand [batch][rows][K] as a 3-D TMA map with a {64, box_rows, 1} box.
+bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, int64_t k, int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * 2), static_cast<cuuint64_t>(rows * k * 2)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void fill_result(const Plan& p, ls_result* r) {
+  std::memset(r, 0, sizeof *r);
+  r->family = p.family;
+  r->status = p.status == P_OK ? LS_RUN_OK
+            : p.status == P_ILLEGAL ? LS_RUN_ILLEGAL
+            : p.status == P_PARSE ? LS_RUN_PARSE
+            : LS_RUN_UNSUPPORTED;
+  std::memcpy(r->cfg, p.cfg, sizeof r->cfg);
+}
+
+}  // namespace
+
+struct ls_runner {
+  int device = 0;
+  ls_runner_opts opts{};
+  cudaStream_t st = nullptr;
+  bool bf16 = false;
+  bool have_workload = false;
+  Workload w;
+  std::string e0_text;
+  bool tc_ok = false;
+  void* x = nullptr;        // device inputs in the runner dtype
+  void* y = nullptr;
+  void* yk = nullptr;       // K-major copy of Y for the tcgen05 family (bf16)
+  float* c = nullptr;
+  double* ref = nullptr;
+  Strides s{};
+  CUtensorMap tmap_a{};
+  std::map<int, CUtensorMap> tmap_b;
+  unsigned long long* deadline = nullptr;  // [0] armed deadline
+  int* flags = nullptr;                    // per-candidate timeout flags
+  unsigned long long* parity = nullptr;    // per-candidate (max err bits, mismatches)
+  int cap = 0;
+  std::vector<cudaEvent_t> ev;             // 4 per candidate slot
+  float last_ms = 0.f;
+  int64_t launches = 0;
+  DeviceLimits lim;
+
+  ~ls_runner() { release(); }
+
+  void release_workload() {
+    cudaFree(x); cudaFree(y); cudaFree(yk); cudaFree(c); cudaFree(ref);
+    x = y = yk = nullptr; c = nullptr; ref = nullptr;
+    tmap_b.clear();
+    have_workload = false;
+  }
+  void release() {
+    cudaSetDevice(device);
+    if (st) cudaStreamSynchronize(st);
+    release_workload();
+    cudaFree(deadline); cudaFree(flags); cudaFree(parity);
+    deadline = nullptr; flags = nullptr; parity = nullptr;
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+    if (st) cudaStreamDestroy(st);
+    st = nullptr;
+  }
+
+  ls_status ensure_capacity(int n) {
+    if (n <= cap) return LS_OK;
+    int nc = std::max(n, 2 * cap);
+    cudaFree(flags);
+    cudaFree(parity);
+    flags = nullptr;
+    parity = nullptr;
+    LSB_CUDA(cudaMalloc(&flags, static_cast<size_t>(nc) * sizeof(int)));
+    LSB_CUDA(cudaMalloc(&parity, static_cast<size_t>(nc) * 2 * sizeof(unsigned long long)));
+    while (ev.size() < static_cast<size_t>(nc) * 4) {
+      cudaEvent_t e;
+      LSB_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    cap = nc;
+    return LS_OK;
+  }
+
+  const CUtensorMap* map_b(int bn) {
+    auto it = tmap_b.find(bn);
+    if (it != tmap_b.end()) return &it->second;
+    CUtensorMap m;
+    if (!make_kmajor_map(&m, yk, w.extent[R_BATCH], w.extent[R_N], w.extent[R_K], bn)) return nullptr;
+    return &(tmap_b[bn] = m);
+  }
+
+  // one launch of a planned candidate (plus its zeroing memset)
+  bool launch(const Plan& p, bool guarded, int slot) {
+    const unsigned long long* dl = guarded ? deadline : nullptr;
+    int* flag = flags + slot;
+    const size_t cbytes = static_cast<size_t>(w.c_elems) * sizeof(float);
+    if (p.needs_zero && cudaMemsetAsync(c, 0, cbytes, st) != cudaSuccess) return false;
+    ++launches;
+    switch (p.family) {
+      case F_NAIVE:
+        launch_naive(x, y, c, s, bf16, st);
+        return cudaGetLastError() == cudaSuccess;
+      case F_SIMT:
+        return launch_simt(x, y, c, s, p.simt, bf16, dl, flag, st);
+      case F_LOOPNEST:
+        launch_loopnest(x, y, c, p.nest, bf16, dl, flag, st);
+        return cudaGetLastError() == cudaSuccess;
+      case F_TC: {
+        const CUtensorMap* mb = map_b(static_cast<int>(p.tc.bn));
+        if (!mb) return false;
+        TcLaunch L;
+        L.tmap_a = &tmap_a;
+        L.tmap_b = mb;
+        L.c = c;
+        L.sc_b = w.sc[R_BATCH];
+        L.sc_m = w.sc[R_M];
+        L.m = static_cast<int>(w.extent[R_M]);
+        L.n = static_cast<int>(w.extent[R_N]);
+        L.k = static_cast<int>(w.extent[R_K]);
+        L.bn = static_cast<int>(p.tc.bn);
+        L.splits = static_cast<int>(p.tc.splits);
+        L.kt = static_cast<int>(p.tc.kt);
+        L.stages = static_cast<int>(p.tc.stages);
+        L.batch = static_cast<int>(p.tc.batch);
+        L.grid_m = static_cast<int>(p.tc.grid_m);
+        L.grid_n = static_cast<int>(p.tc.grid_n);
+        L.accumulate = p.tc.splits > 1;
+        L.smem_bytes = static_cast<int>(p.tc.smem_bytes);
+        return launch_tc_gemm(L, st);
+      }
+      default:
+        return false;
+    }
+  }
+};
+
+namespace {
+
+ls_status plan_all(const Workload& w, const DeviceLimits& lim, const char* const* programs, const size_t* lens, int n,
+                   std::vector<Plan>* plans) {
+  plans->assign(static_cast<size_t>(n), Plan());
+  parallel_for(n, [&](int i) {
+    std::string err;
+    auto p = parse_program(std::string_view(programs[i], lens[i]), &err);
+    Plan& out = (*plans)[static_cast<size_t>(i)];
+    if (!p) {
+      out.status = P_PARSE;
+      out.why = err;
+      return;
+    }
+    out = plan_program(w, *p, lim);
+  });
+  return LS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* programs, const size_t* lens, int n,
+                           int32_t dtype, ls_result* out) {
+  if (!e0 || !out || n < 0 || (n > 0 && (!programs || !lens))) {
+    set_error("ls_plan_programs: bad arguments");
+    return LS_ERR_ARG;
+  }
+  std::string err;
+  auto p0 = parse_program(std::string_view(e0, e0_len), &err);
+  if (!p0) {
+    set_error("e0: " + err);
+    return LS_ERR_PARSE;
+  }
+  Workload w;
+  if (!analyze_workload(*p0, &w, &err)) {
+    set_error("e0: " + err);
+    return LS_ERR_ARG;
+  }
+  DeviceLimits lim;
+  lim.bf16 = dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
+  std::vector<Plan> plans;
+  plan_all(w, lim, programs, lens, n, &plans);
+  for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
+  return LS_OK;
+}
+
+ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** out) {
+  if (!out) {
+    set_error("ls_runner_create: null out");
+    return LS_ERR_ARG;
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device: the B200 runner has no CPU fallback");
+    return LS_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    set_error("device index out of range");
+    return LS_ERR_ARG;
+  }
+  LSB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  LSB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_error("the runner's kernels are compiled for sm_100a (B200)");
+    return LS_ERR_CUDA;
+  }
+  auto r = std::make_unique<ls_runner>();
+  r->device = device;
+  ls_runner_opts o{};
+  o.dtype = LS_DTYPE_BF16;
+  o.min_repeats = 3;
+  o.max_repeats = 200;
+  o.target_ms = 0.2;
+  o.timeout_ms = 2.0;
+  o.rtol = 0.0;
+  o.atol = 0.0;
+  if (opts) o = *opts;
+  if (o.min_repeats < 1) o.min_repeats = 1;
+  if (o.max_repeats < o.min_repeats) o.max_repeats = o.min_repeats;
+  r->opts = o;
+  r->bf16 = o.dtype == LS_DTYPE_BF16;
+  r->lim.max_threads = prop.maxThreadsPerBlock;
+  r->lim.max_smem = static_cast<int64_t>(prop.sharedMemPerBlockOptin) - 1024;
+  LSB_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  LSB_CUDA(cudaMalloc(&r->deadline, 2 * sizeof(unsigned long long)));
+  ls_status s = r->ensure_capacity(256);
+  if (s != LS_OK) return s;
+  *out = r.release();
+  return LS_OK;
+}
+
+ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const float* const* host_inputs,
+                                 int n_inputs) {
+  if (!r || !e0 || !host_inputs) {
+    set_error("ls_runner_set_workload: bad arguments");
+    return LS_ERR_ARG;
+  }
+  LSB_CUDA(cudaSetDevice(r->device));
+  LSB_CUDA(cudaStreamSynchronize(r->st));
+  r->release_workload();
+  std::string err;
+  auto p0 = parse_program(std::string_view(e0, len), &err);
+  if (!p0) {
+    set_error("e0: " + err);
+    return LS_ERR_PARSE;
+  }
+  Workload w;
+  if (!analyze_workload(*p0, &w, &err)) {
+    set_error("e0: " + err);
+    return LS_ERR_ARG;
+  }
+  if (static_cast<int>(w.input_bufs.size()) != n_inputs) {
+    set_error("ls_runner_set_workload: input count does not match the program's input buffers");
+    return LS_ERR_ARG;
+  }
+  r->w = w;
+  r->e0_text.assign(e0, len);
+  for (int i = 0; i < 4; ++i) {
+    r->s.sx[i] = w.sx[i];
+    r->s.sy[i] = w.sy[i];
+    r->s.sc[i] = w.sc[i];
+    r->s.ext[i] = w.extent[i];
+  }
+  const size_t es = r->bf16 ? 2 : 4;
+  auto upload = [&](int buf, int64_t elems, void** dst) -> ls_status {
+    int idx = -1;
+    for (int i = 0; i < n_inputs; ++i)
+      if (w.input_bufs[static_cast<size_t>(i)] == buf) idx = i;
+    if (idx < 0) {
+      set_error("operand is not an input buffer");
+      return LS_ERR_ARG;
+    }
+    LSB_CUDA(cudaMalloc(dst, static_cast<size_t>(elems) * es));
+    if (!r->bf16) {
+      LSB_CUDA(cudaMemcpyAsync(*dst, host_inputs[idx], static_cast<size_t>(elems) * 4, cudaMemcpyHostToDevice, r->st));
+    } else {
+      float* tmp = nullptr;
+      LSB_CUDA(cudaMalloc(&tmp, static_cast<size_t>(elems) * 4));
+      LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[idx], static_cast<size_t>(elems) * 4, cudaMemcpyHostToDevice, r->st));
+      launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(*dst), elems, r->st);
+      LSB_CUDA(cudaStreamSynchronize(r->st));
+      cudaFree(tmp);
+    }
+    return LS_OK;
+  };
+  ls_status s;
+  if ((s = upload(w.x_buf, w.x_elems, &r->x)) != LS_OK) return s;
+  if ((s = upload(w.y_buf, w.y_elems, &r->y)) != LS_OK) return s;
+  LSB_CUDA(cudaMalloc(&r->c, static_cast<size_t>(w.c_elems) * 4));
+  LSB_CUDA(cudaMalloc(&r->ref, static_cast<size_t>(w.c_elems) * 8));
+  launch_reference(r->x, r->y, r->ref, r->s, r->bf16, r->st);
+  LSB_CUDA(cudaGetLastError());
+
+  // tcgen05 operands: X must be [batch][M][K]; Y is used K-major ([batch][N][K]),
+  // transposed once here when the workload stores it [batch][K][N].
+  const int64_t B = w.extent[R_BATCH], M = w.extent[R_M], N = w.extent[R_N], K = w.extent[R_K];
+  bool x_ok = w.x_kmajor && w.sx[R_M] == K && (!w.has_batch || w.sx[R_BATCH] == M * K);
+  bool y_kmaj = w.y_kmajor && w.sy[R_N] == K && (!w.has_batch || w.sy[R_BATCH] == N * K);
+  bool y_nmaj = !w.y_kmajor && w.sy[R_N] == 1 && w.sy[R_K] == N && (!w.has_batch || w.sy[R_BATCH] == N * K);
+  bool c_ok = w.sc[R_N] == 1 && w.sc[R_M] == N && (!w.has_batch || w.sc[R_BATCH] == M * N);
+  r->tc_ok = r->bf16 && x_ok && (y_kmaj || y_nmaj) && c_ok && K % 64 == 0 && M % 128 == 0;
+  if (r->tc_ok) {
+    if (y_kmaj) {
+      r->yk = nullptr;
+      LSB_CUDA(cudaMalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
+      LSB_CUDA(cudaMemcpyAsync(r->yk, r->y, static_cast<size_t>(w.y_elems) * 2, cudaMemcpyDeviceToDevice, r->st));
+    } else {
+      LSB_CUDA(cudaMalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
+      launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->y), static_cast<__nv_bfloat16*>(r->yk), B, K, N,
+                            r->st);
+      LSB_CUDA(cudaGetLastError());
+    }
+    if (!make_kmajor_map(&r->tmap_a, r->x, B, M, K, 128)) {
+      set_error("cuTensorMapEncodeTiled failed for the A operand");
+      return LS_ERR_CUDA;
+    }
+  }
+  r->lim.bf16 = r->tc_ok;
+  LSB_CUDA(cudaStreamSynchronize(r->st));
+  r->have_workload = true;
+  return LS_OK;
+}
+
+ls_status ls_runner_plan(ls_runner* r, const char* const* programs, const size_t* lens, int n, ls_result* out) {
+  if (!r || !r->have_workload) {
+    set_error("ls_runner_plan: no workload");
+    return LS_ERR_STATE;
+  }
+  std::vector<Plan> plans;
+  plan_all(r->w, r->lim, programs, lens, n, &plans);
+  for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
+  return LS_OK;
+}
+
+ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const size_t* lens, int n, ls_result* out) {
+  if (!r || !out || n < 0 || (n > 0 && (!programs || !lens))) {
+    set_error("ls_runner_measure: bad arguments");
+    return LS_ERR_ARG;
+  }
+  if (!r->have_workload) {
+    set_error("ls_runner_measure: set a workload first");
+    return LS_ERR_STATE;
+  }
+  LSB_CUDA(cudaSetDevice(r->device));
+  ls_status s = r->ensure_capacity(n);
+  if (s != LS_OK) return s;
+  std::vector<Plan> plans;
+  plan_all(r->w, r->lim, programs, lens, n, &plans);
+  for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
+  r->launches = 0;
+  const size_t cbytes = static_cast<size_t>(r->w.c_elems) * sizeof(float);
+  const unsigned long long timeout_ns = static_cast<unsigned long long>(r->opts.timeout_ms * 1e6);
+  LSB_CUDA(cudaMemsetAsync(r->flags, 0, static_cast<size_t>(n) * sizeof(int), r->st));
+  LSB_CUDA(cudaMemsetAsync(r->parity, 0, static_cast<size_t>(n) * 16, r->st));
+  cudaEvent_t* E = r->ev.data();
+  cudaEvent_t batch0;
+  LSB_CUDA(cudaEventCreate(&batch0));
+  LSB_CUDA(cudaEventRecord(batch0, r->st));
+
+  // ---- phase A: checked run ----
+  std::vector<char> launched(static_cast<size_t>(n), 0);
+  for (int i = 0; i < n; ++i) {
+    const Plan& p = plans[static_cast<size_t>(i)];
+    if (p.status != P_OK) continue;
+    LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));  // NaN poison: unwritten outputs fail parity
+    launch_set_deadline(r->deadline, timeout_ns, r->st);
+    ++r->launches;
+    LSB_CUDA(cudaEventRecord(E[4 * i], r->st));
+    bool ok = r->launch(p, true, i);
+    LSB_CUDA(cudaEventRecord(E[4 * i + 1], r->st));
+    if (!ok) {
+      cudaGetLastError();
+      out[i].status = LS_RUN_LAUNCH;
+      continue;
+    }
+    launch_parity(r->c, r->ref, r->w.c_elems, r->opts.rtol, r->opts.atol, r->parity + 2 * i, r->st);
+    ++r->launches;
+    launched[static_cast<size_t>(i)] = 1;
+  }
+  cudaError_t se = cudaStreamSynchronize(r->st);
+  if (se != cudaSuccess) {
+    cudaEventDestroy(batch0);
+    set_error(std::string("runner phase A: ") + cudaGetErrorString(se));
+    return LS_ERR_CUDA;
+  }
+  std::vector<int> tflag(static_cast<size_t>(n));
+  std::vector<unsigned long long> par(static_cast<size_t>(2 * n));
+  LSB_CUDA(cudaMemcpy(tflag.data(), r->flags, static_cast<size_t>(n) * sizeof(int), cudaMemcpyDeviceToHost));
+  LSB_CUDA(cudaMemcpy(par.data(), r->parity, static_cast<size_t>(n) * 16, cudaMemcpyDeviceToHost));
+  std::vector<float> warm(static_cast<size_t>(n), 0.f);
+  for (int i = 0; i < n; ++i) {
+    if (!launched[static_cast<size_t>(i)]) continue;
+    LSB_CUDA(cudaEventElapsedTime(&warm[static_cast<size_t>(i)], E[4 * i], E[4 * i + 1]));
+    double err;
+    unsigned long long bits = par[static_cast<size_t>(2 * i)];
+    std::memcpy(&err, &bits, sizeof err);
+    out[i].max_abs_err = err;
+    out[i].mismatches = static_cast<int64_t>(par[static_cast<size_t>(2 * i + 1)]);
+    if (tflag[static_cast<size_t>(i)]) {
+      out[i].status = LS_RUN_TIMEOUT;
+      out[i].latency_ns = r->opts.timeout_ms * 1e6;
+      out[i].repeats = 1;
+      launched[static_cast<size_t>(i)] = 0;
+    } else if (out[i].mismatches) {
+      out[i].status = LS_RUN_PARITY;
+    }
+  }
+
+  // ---- phase B: timed repeats, chunked behind a device spin ----
+  std::vector<int> reps(static_cast<size_t>(n), 0);
+  const int chunk = 32;
+  double prev_gpu_us = 0.0;
+  for (int c0 = 0; c0 < n; c0 += chunk) {
+    int c1 = std::min(n, c0 + chunk);
+    int64_t calls = 0;
+    double gpu_us = 0.0;
+    for (int i = c0; i < c1; ++i) {
+      if (!launched[static_cast<size_t>(i)]) continue;
+      double wm = std::max(1e-4, static_cast<double>(warm[static_cast<size_t>(i)]));
+      int rep = static_cast<int>(std::ceil(r->opts.target_ms / wm));
+      rep = std::max(r->opts.min_repeats, std::min(r->opts.max_repeats, rep));
+      reps[static_cast<size_t>(i)] = rep;
+      calls += rep * (plans[static_cast<size_t>(i)].needs_zero ? 2 : 1) + 2;
+      gpu_us += rep * wm * 1e3;
+    }
+    if (!calls) continue;
+    double host_us = 4.0 * static_cast<double>(calls);
+    double spin = host_us - prev_gpu_us;
+    if (spin > 0) {
+      launch_delay(static_cast<unsigned long long>(std::min(spin, 20000.0) * 1e3), r->st);
+      ++r->launches;
+    }
+    for (int i = c0; i < c1; ++i) {
+      if (!launched[static_cast<size_t>(i)]) continue;
+      const Plan& p = plans[static_cast<size_t>(i)];
+      LSB_CUDA(cudaEventRecord(E[4 * i + 2], r->st));
+      for (int k = 0; k < reps[static_cast<size_t>(i)]; ++k)
+        if (!r->launch(p, false, i)) {
+          set_error("runner phase B: launch failed");
+          cudaEventDestroy(batch0);
+          return LS_ERR_CUDA;
+        }
+      LSB_CUDA(cudaEventRecord(E[4 * i + 3], r->st));
+    }
+    prev_gpu_us = gpu_us;
+  }
+  cudaEvent_t batch1;
+  LSB_CUDA(cudaEventCreate(&batch1));
+  LSB_CUDA(cudaEventRecord(batch1, r->st));
+  se = cudaStreamSynchronize(r->st);
+  if (se != cudaSuccess) {
+    set_error(std::string("runner phase B: ") + cudaGetErrorString(se));
+    return LS_ERR_CUDA;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!launched[static_cast<size_t>(i)]) continue;
+    float ms = 0.f;
+    LSB_CUDA(cudaEventElapsedTime(&ms, E[4 * i + 2], E[4 * i + 3]));
+    out[i].repeats = reps[static_cast<size_t>(i)];
+    out[i].latency_ns = 1e6 * static_cast<double>(ms) / reps[static_cast<size_t>(i)];
+  }
+  cudaEventElapsedTime(&r->last_ms, batch0, batch1);
+  cudaEventDestroy(batch0);
+  cudaEventDestroy(batch1);
+  return LS_OK;
+}
+
+ls_status ls_runner_baseline(ls_runner* r, ls_result* out) {
+  if (!r || !r->have_workload) {
+    set_error("ls_runner_baseline: no workload");
+    return LS_ERR_STATE;
+  }
+  const char* t = r->e0_text.c_str();
+  size_t l = r->e0_text.size();
+  return ls_runner_measure(r, &t, &l, 1, out);
+}
+
+ls_status ls_runner_last_output(ls_runner* r, float* host, size_t count) {
+  if (!r || !r->have_workload || !host || count > static_cast<size_t>(r->w.c_elems)) {
+    set_error("ls_runner_last_output: bad arguments");
+    return LS_ERR_ARG;
+  }
+  LSB_CUDA(cudaSetDevice(r->device));
+  LSB_CUDA(cudaStreamSynchronize(r->st));
+  LSB_CUDA(cudaMemcpy(host, r->c, count * 4, cudaMemcpyDeviceToHost));
+  return LS_OK;
+}
+
+ls_status ls_runner_reference_output(ls_runner* r, double* host, size_t count) {
+  if (!r || !r->have_workload || !host || count > static_cast<size_t>(r->w.c_elems)) {
+    set_error("ls_runner_reference_output: bad arguments");
+    return LS_ERR_ARG;
+  }
+  LSB_CUDA(cudaSetDevice(r->device));
+  LSB_CUDA(cudaStreamSynchronize(r->st));
+  LSB_CUDA(cudaMemcpy(host, r->ref, count * 8, cudaMemcpyDeviceToHost));
+  return LS_OK;
+}
+
+ls_status ls_runner_elapsed_ms(ls_runner* r, float* ms) {
+  if (!r || !ms) {
+    set_error("ls_runner_elapsed_ms: bad arguments");
+    return LS_ERR_ARG;
+  }
+  *ms = r->last_ms;
+  return LS_OK;
+}
+
+ls_status ls_runner_launch_count(ls_runner* r, int64_t* count) {
+  if (!r || !count) {
+    set_error("ls_runner_launch_count: bad arguments");
+    return LS_ERR_ARG;
+  }
+  *count = r->launches;
+  return LS_OK;
+}
+
+void ls_runner_destroy(ls_runner* r) { delete r; }
+
+}  // extern "C"

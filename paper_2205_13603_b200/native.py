@@ -1,0 +1,204 @@
+"""ctypes binding of the C ABI in ``include/loopsched_b200.h``.
+
+The shared library ``_lib/libls_b200.so`` is built in-tree by
+``__graft_entry__.build()`` (``make -C paper_2205_13603_b200/csrc``).  Loading
+fails loudly when it is missing -- there is no CPU fallback for any compute
+entry point.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libls_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_f64p = ctypes.POINTER(ctypes.c_double)
+c_f32p = ctypes.POINTER(ctypes.c_float)
+
+
+class MachineSpecC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("cores", "vector_lanes", "cache_capacity", "hit_cost", "miss_cost",
+                 "flop_cost", "tensor_unit_cost", "unroll_num", "unroll_den")]
+
+
+class LinearModelC(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_double * 9), ("mean", ctypes.c_double * 9),
+                ("scale", ctypes.c_double * 9), ("intercept", ctypes.c_double),
+                ("n_records", ctypes.c_int64), ("is_fit", ctypes.c_int32)]
+
+
+class RunnerOptsC(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("min_repeats", ctypes.c_int32),
+                ("max_repeats", ctypes.c_int32), ("target_ms", ctypes.c_double),
+                ("timeout_ms", ctypes.c_double), ("rtol", ctypes.c_double),
+                ("atol", ctypes.c_double), ("flush_l2", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 7)]
+
+
+class ResultC(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("family", ctypes.c_int32),
+                ("repeats", ctypes.c_int32), ("cfg", ctypes.c_int32 * 13),
+                ("latency_ns", ctypes.c_double), ("max_abs_err", ctypes.c_double),
+                ("mismatches", ctypes.c_int64)]
+
+
+EXPORTS = {
+    # name: (restype, argtypes)
+    "ls_sim_latency_batch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                            ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                            ctypes.POINTER(MachineSpecC), c_i64p, c_i64p, c_i32p]),
+    "ls_featurize_batch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                          ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                          ctypes.POINTER(MachineSpecC), c_f64p, c_i32p]),
+    "ls_score_batch": (ctypes.c_int, [ctypes.c_int, c_f64p, ctypes.c_int,
+                                      ctypes.POINTER(LinearModelC), c_f64p]),
+    "ls_analyze_batch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                        ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                        ctypes.POINTER(MachineSpecC), ctypes.POINTER(LinearModelC),
+                                        c_i64p, c_i64p, c_f64p, c_f64p, c_i32p]),
+    "ls_batch_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
+                                       ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_void_p)]),
+    "ls_batch_analyze": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(MachineSpecC),
+                                        ctypes.POINTER(LinearModelC), ctypes.c_int]),
+    "ls_batch_results": (ctypes.c_int, [ctypes.c_void_p, c_i64p, c_i64p, c_f64p, c_f64p, c_i32p]),
+    "ls_batch_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, c_f32p]),
+    "ls_batch_destroy": (None, [ctypes.c_void_p]),
+    "ls_runner_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(RunnerOptsC),
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "ls_runner_set_workload": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t,
+                                              ctypes.POINTER(c_f32p), ctypes.c_int]),
+    "ls_runner_measure": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                         ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                         ctypes.POINTER(ResultC)]),
+    "ls_runner_baseline": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ResultC)]),
+    "ls_runner_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                      ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                      ctypes.POINTER(ResultC)]),
+    "ls_plan_programs": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t,
+                                        ctypes.POINTER(ctypes.c_char_p),
+                                        ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                        ctypes.c_int32, ctypes.POINTER(ResultC)]),
+    "ls_runner_last_output": (ctypes.c_int, [ctypes.c_void_p, c_f32p, ctypes.c_size_t]),
+    "ls_runner_reference_output": (ctypes.c_int, [ctypes.c_void_p, c_f64p, ctypes.c_size_t]),
+    "ls_runner_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, c_f32p]),
+    "ls_runner_launch_count": (ctypes.c_int, [ctypes.c_void_p, c_i64p]),
+    "ls_runner_destroy": (None, [ctypes.c_void_p]),
+    "ls_last_error": (ctypes.c_char_p, []),
+    "ls_version": (ctypes.c_char_p, []),
+}
+
+STATUS = {0: "OK", 1: "ILLEGAL", 2: "UNSUPPORTED", 3: "PARSE", 4: "LAUNCH", 5: "PARITY",
+          6: "TIMEOUT"}
+FAMILY = {0: "none", 1: "naive", 2: "simt", 3: "tcgen05", 4: "loopnest"}
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def build(verbose: bool = False) -> str:
+    jobs = str(max(1, min(8, os.cpu_count() or 1)))
+    subprocess.run(["make", "-s", "-j", jobs, "-C", CSRC], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """The loaded library; raises when it was never built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the B200 path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != 0:
+        msg = lib().ls_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (status {status}): {msg}")
+
+
+def text_array(programs):
+    enc = [p.encode() if isinstance(p, str) else bytes(p) for p in programs]
+    n = len(enc)
+    arr = (ctypes.c_char_p * max(n, 1))(*enc)
+    lens = (ctypes.c_size_t * max(n, 1))(*[len(b) for b in enc])
+    return arr, lens, enc
+
+
+def machine_spec_c(spec=None) -> MachineSpecC:
+    """From a reference MachineSpec, a dict, or None (defaults of
+    `src/machine.py:22-31`)."""
+    d = {"cores": 4, "vector_lanes": 8, "cache_capacity": 4096, "hit_cost": 1,
+         "miss_cost": 8, "flop_cost": 1, "unroll_discount": 0.9, "tensor_unit_cost": 8}
+    if spec is not None:
+        src = spec if isinstance(spec, dict) else spec.to_json()
+        d.update(src)
+    disc = Fraction(str(d["unroll_discount"]))
+    return MachineSpecC(d["cores"], d["vector_lanes"], d["cache_capacity"], d["hit_cost"],
+                        d["miss_cost"], d["flop_cost"], d["tensor_unit_cost"],
+                        disc.numerator, disc.denominator)
+
+
+def linear_model_c(model) -> LinearModelC:
+    """From a reference CostModel or a dict with the same field names."""
+    get = (lambda k, dflt=None: model.get(k, dflt)) if isinstance(model, dict) \
+        else (lambda k, dflt=None: getattr(model, k, dflt))
+    m = LinearModelC()
+    w = get("weights")
+    m.is_fit = 1 if w is not None else 0
+    if w is not None:
+        mean, scale = get("feature_mean"), get("feature_scale")
+        for i in range(9):
+            m.w[i] = float(w[i])
+            m.mean[i] = float(mean[i])
+            m.scale[i] = float(scale[i])
+    m.intercept = float(get("intercept", 0.0) or 0.0)
+    m.n_records = int(get("n_records", 0) or 0)
+    return m
+
+
+def results_to_dicts(res, n):
+    out = []
+    for i in range(n):
+        r = res[i]
+        out.append({"status": STATUS.get(r.status, str(r.status)), "family": FAMILY.get(r.family, "?"),
+                    "repeats": r.repeats, "cfg": list(r.cfg), "latency_ns": r.latency_ns,
+                    "max_abs_err": r.max_abs_err, "mismatches": r.mismatches})
+    return out
+
+
+def plan_programs(e0: str, programs, dtype: str = "bf16"):
+    """Host-only instantiation of each program (no GPU needed)."""
+    arr, lens, _keep = text_array(programs)
+    n = len(programs)
+    res = (ResultC * max(n, 1))()
+    e = e0.encode()
+    check(lib().ls_plan_programs(e, len(e), arr, lens, n, 1 if dtype == "bf16" else 0, res),
+          "ls_plan_programs")
+    return results_to_dicts(res, n)
+
+
+def as_np_ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
