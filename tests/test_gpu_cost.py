@@ -1,0 +1,80 @@
+"""K7 (featurize + score) and K8 (exact simulated latency) on the B200 against
+the oracle and the reference's golden outputs."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from conftest import load_model, load_population, load_programs
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def scorer():
+    from paper_2205_13603_b200.scorer import GpuScorer
+    return GpuScorer(0)
+
+
+def test_k8_latency_bit_exact_on_goldens(scorer):
+    rows = load_programs()
+    lats = scorer.sim_latency_batch([r["program"] for r in rows])
+    for r, l in zip(rows, lats):
+        assert l == Fraction(*r["latency"]), r["name"]
+        assert l == O.sim_latency(r["program"])
+
+
+@pytest.mark.parametrize("name", ["bert_ffn", "bmm_qk", "gmm512", "conv2d"])
+def test_k8_k7_on_populations(scorer, name):
+    hdr, pop = load_population(name)
+    pop = pop[:1024]
+    lats, feats, _ = scorer.analyze([p["program"] for p in pop])
+    assert all(l == Fraction(*p["latency"]) for l, p in zip(lats, pop))
+    ref = np.array([p["features"] for p in pop])
+    # log1p on the GPU may differ from glibc by 1 ulp; everything else is exact
+    np.testing.assert_allclose(feats, ref, rtol=1e-14, atol=0)
+    assert (feats == ref).mean() > 0.9
+
+
+def test_k7_features_and_scores(scorer):
+    rows = load_programs()
+    model = load_model()
+    _, feats, pred = scorer.analyze([r["program"] for r in rows], model=model)
+    F = np.array([r["features"] for r in rows])
+    np.testing.assert_allclose(feats, F, rtol=1e-14, atol=0)
+    P = np.array([r["predicted"] for r in rows])
+    np.testing.assert_allclose(pred, P, rtol=1e-5)   # north_star tolerance
+    np.testing.assert_allclose(pred, P, rtol=1e-12)  # what we actually get
+    s = scorer.score_batch(F, model)
+    np.testing.assert_allclose(s, P, rtol=1e-12)
+    for f, p in zip(F[:20], s[:20]):
+        assert p == pytest.approx(O.predict(f, model), rel=1e-12)
+
+
+def test_unfit_and_warm_models(scorer):
+    F = np.zeros((3, 9))
+    assert np.all(scorer.score_batch(F, {"weights": None}) == 1.0)
+    warm = {"weights": None, "intercept": float(np.log(8.0)), "n_records": 2}
+    np.testing.assert_allclose(scorer.score_batch(F, warm), 8.0)
+
+
+def test_device_batch_matches_one_shot(scorer):
+    from paper_2205_13603_b200.scorer import DeviceBatch
+    hdr, pop = load_population("gmm512")
+    texts = [p["program"] for p in pop[:256]]
+    model = load_model()
+    b = DeviceBatch(texts)
+    b.analyze(model=model)
+    num, den, feats, pred, st = b.results()
+    assert b.elapsed_ms() > 0
+    lats, f2, p2 = scorer.analyze(texts, model=model)
+    assert (st == 0).all()
+    assert [Fraction(int(a), int(c)) for a, c in zip(num, den)] == lats
+    assert np.array_equal(feats, f2) and np.array_equal(pred, p2)
+
+
+def test_parse_failure_is_reported(scorer):
+    from paper_2205_13603_b200.scorer import AnalysisError
+    with pytest.raises(AnalysisError):
+        scorer.analyze(["{bad json"])

@@ -1,0 +1,139 @@
+"""The hardware Runner: every candidate's output against the oracle, per
+kernel family, at the BASELINE shapes; float tolerance checks; statuses."""
+import numpy as np
+import pytest
+
+from conftest import load_population
+from oracle import oracle as O
+from paper_2205_13603_b200.inputs import normal_inputs, random_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def make_runner(dtype, **kw):
+    from paper_2205_13603_b200.runner import B200Runner
+    kw.setdefault("min_repeats", 1)
+    kw.setdefault("max_repeats", 3)
+    kw.setdefault("target_ms", 0.005)
+    return B200Runner(device=0, dtype=dtype, **kw)
+
+
+def pick(plans, family, k):
+    return [i for i, p in enumerate(plans) if p["family"] == family and p["status"] == "OK"][:k]
+
+
+@pytest.mark.parametrize("name,dtype", [("bert_ffn", "bf16"), ("bmm_qk", "bf16"), ("gmm512", "f32"),
+                                        ("bmm_qk", "f32")])
+def test_reference_output_is_exact(name, dtype):
+    hdr, _ = load_population(name)
+    e0 = hdr["e0"]
+    r = make_runner(dtype)
+    r.set_workload(e0, seed=0)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 0)).values()))
+    assert np.array_equal(r.reference_output(), want)
+    r.close()
+
+
+@pytest.mark.parametrize("name,dtype,families", [
+    ("bert_ffn", "bf16", ("tcgen05", "simt", "naive")),
+    ("bmm_qk", "bf16", ("tcgen05", "simt")),
+    ("gmm512", "f32", ("simt",)),
+])
+def test_candidates_bit_exact_per_family(name, dtype, families):
+    hdr, pop = load_population(name)
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop[:1024]] + [e0]
+    r = make_runner(dtype, timeout_ms=50.0)
+    r.set_workload(e0, seed=0)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 0)).values()))
+    plans = r.plan_programs(progs)
+    for fam in families:
+        idx = pick(plans, fam, 12 if fam != "naive" else 1)
+        assert idx, fam
+        for i in idx:
+            res, = r.measure_programs([progs[i]])
+            assert res["status"] == "OK", (fam, res)
+            assert res["mismatches"] == 0 and res["max_abs_err"] == 0.0
+            assert np.array_equal(r.last_output().astype(np.float64), want), (fam, res["cfg"])
+    r.close()
+
+
+def test_all_tcgen05_candidates_exact_bert_ffn():
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    r = make_runner("bf16")
+    r.set_workload(e0, seed=1)
+    plans = r.plan_programs(progs)
+    idx = pick(plans, "tcgen05", 10 ** 6)
+    res = r.measure_programs([progs[i] for i in idx])
+    assert len(res) > 100
+    for x in res:
+        assert x["status"] == "OK" and x["mismatches"] == 0, x
+        assert x["latency_ns"] > 0 and x["repeats"] >= 1
+    r.close()
+
+
+def test_float_inputs_tolerance():
+    # N(0,1) inputs: fp32 candidates within rtol 1e-4 of fp64 math; bf16 inputs
+    # are rounded once at upload, the candidates then accumulate in fp32.
+    for name, dtype, rtol in (("gmm512", "f32", 1e-4), ("bert_ffn", "bf16", 2e-2)):
+        hdr, pop = load_population(name)
+        e0 = hdr["e0"]
+        ins = normal_inputs(e0, 7)
+        r = make_runner(dtype, rtol=rtol, atol=1e-3)
+        r.set_workload(e0, inputs=ins)
+        ref = r.reference_output()
+        cast = {k: (v.astype(np.float32) if dtype == "f32" else
+                    _bf16(v)) for k, v in ins.items()}
+        want = next(iter(O.reference_outputs(e0, cast).values()))
+        np.testing.assert_allclose(ref, want, rtol=1e-9, atol=1e-9)
+        plans = r.plan_programs([p["program"] for p in pop[:600]])
+        for fam in ("simt", "tcgen05"):
+            for i in pick(plans, fam, 4):
+                res, = r.measure_programs([pop[i]["program"]])
+                assert res["status"] == "OK", res
+                out = r.last_output().astype(np.float64)
+                np.testing.assert_allclose(out, want, rtol=rtol, atol=1e-3)
+        r.close()
+
+
+def _bf16(v):
+    import torch
+    return torch.tensor(v, dtype=torch.float32).to(torch.bfloat16).to(torch.float32).numpy()
+
+
+def test_statuses_and_sentinels():
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    r = make_runner("bf16", timeout_ms=0.05)
+    r.set_workload(e0, seed=0)
+    progs = [p["program"] for p in pop[:400]]
+    plans = r.plan_programs(progs)
+    ill = [i for i, p in enumerate(plans) if p["status"] == "ILLEGAL"][:3]
+    nest = [i for i, p in enumerate(plans) if p["family"] == "loopnest"][:1]
+    res = r.measure_programs([progs[i] for i in ill + nest] + ["{bad"])
+    assert [x["status"] for x in res[:len(ill)]] == ["ILLEGAL"] * len(ill)
+    if nest:
+        assert res[len(ill)]["status"] == "TIMEOUT"  # the PVU row-per-thread nest takes ms
+    assert res[-1]["status"] == "PARSE"
+    lats = r.latencies(res)
+    base = r.baseline()
+    assert all(l == base * 10 ** 4 for l in lats)  # finite sentinel, never inf
+    r.close()
+
+
+def test_measure_signature_matches_reference_runner():
+    from fractions import Fraction
+    hdr, pop = load_population("bmm_qk")
+    r = make_runner("bf16")
+    r.set_workload(hdr["e0"])
+
+    class Cand:  # the reference Candidate's .program attribute (src/search.py:63-69)
+        def __init__(self, p):
+            self.program = p
+
+    out = r.measure([Cand(p["program"]) for p in pop[:8]], None, 1)
+    assert len(out) == 8 and all(isinstance(x, Fraction) and x > 0 for x in out)
+    assert isinstance(r.baseline(), Fraction)
+    r.close()

@@ -1,0 +1,78 @@
+"""Host-side instantiator (trace program -> kernel family + config)."""
+import json
+from collections import Counter
+
+import pytest
+
+from conftest import load_population
+from paper_2205_13603_b200 import native
+
+
+def plan(e0, progs, dtype="bf16"):
+    return native.plan_programs(e0, progs, dtype)
+
+
+def test_e0_maps_to_naive():
+    hdr, _ = load_population("bert_ffn")
+    r, = plan(hdr["e0"], [hdr["e0"]])
+    assert (r["family"], r["status"]) == ("naive", "OK")
+
+
+def test_population_families_bert_ffn():
+    hdr, pop = load_population("bert_ffn")
+    res = plan(hdr["e0"], [p["program"] for p in pop[:1024]])
+    c = Counter((r["family"], r["status"]) for r in res)
+    assert c[("tcgen05", "OK")] > 40
+    assert c[("simt", "OK")] > 100
+    assert c[("loopnest", "OK")] >= 1
+    for r in res:
+        if r["family"] == "tcgen05":
+            batch, gm, gn, bn, splits, kt, stages, smem_kb = r["cfg"][:8]
+            assert gm * 128 == 128 and gn * bn == 768 and splits * kt * 64 == 3072
+            assert (r["status"] == "OK") == (bn <= 256)
+            assert 1 <= stages <= min(kt, 8)
+
+
+def test_fp32_has_no_tensor_core_family():
+    hdr, pop = load_population("bert_ffn")
+    res = plan(hdr["e0"], [p["program"] for p in pop[:300]], dtype="f32")
+    assert not any(r["family"] == "tcgen05" for r in res)
+
+
+def test_simt_mapping_matches_mlt_bands():
+    # MLT SSRSR on gmm: i0 j0 | i1 j1 | k0 | i2 j2 | k1 -> grid/threads/registers
+    hdr, pop = load_population("gmm512")
+    res = plan(hdr["e0"], [p["program"] for p in pop[:200]], dtype="f32")
+    for p, r in zip(pop[:200], res):
+        if r["family"] != "simt":
+            continue
+        gb, gm, gn, tb, tm, tn, rb, rm, rn, bk, kt = r["cfg"][:11]
+        assert gm * tm * rm == 512 and gn * tn * rn == 512 and bk * kt == 512
+        assert (gb, tb, rb) == (1, 1, 1)
+        legal = tm * tn <= 1024 and rm * rn <= 64 and rm in (1, 2, 3, 4, 6, 8, 12, 16) \
+            and rn in (1, 2, 3, 4, 6, 8, 12, 16) and bk * (tm * rm + tn * rn) * 4 <= 231 * 1024
+        assert (r["status"] == "OK") == legal, r
+
+
+def test_bmm_batch_axis_mapping():
+    hdr, pop = load_population("bmm_qk")
+    res = plan(hdr["e0"], [p["program"] for p in pop[:300]])
+    for r in res:
+        if r["family"] == "simt" and r["status"] == "OK":
+            gb, gm, gn, tb, tm, tn, rb, rm, rn, bk, kt = r["cfg"][:11]
+            assert gb * tb * rb == 12 and gm * tm * rm == 128 and gn * tn * rn == 128
+        if r["family"] == "tcgen05":
+            assert r["cfg"][0] == 12 and r["status"] == "OK"
+
+
+def test_unsupported_workload_is_reported():
+    hdr, pop = load_population("conv2d")
+    with pytest.raises(native.NativeError, match="single-block"):
+        plan(hdr["e0"], [pop[0]["program"]])
+
+
+def test_parse_errors_are_per_candidate():
+    hdr, pop = load_population("bmm_qk")
+    res = plan(hdr["e0"], ["{not json", pop[0]["program"]])
+    assert res[0]["status"] == "PARSE"
+    assert res[1]["status"] in ("OK", "ILLEGAL")
