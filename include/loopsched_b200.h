@@ -145,6 +145,15 @@ ls_status ls_runner_reference_output(ls_runner* r, double* host, size_t count);
 ls_status ls_runner_elapsed_ms(ls_runner* r, float* ms);
 /* Kernel launches (candidates + parity/deadline/spin helpers) of the last measure call. */
 ls_status ls_runner_launch_count(ls_runner* r, int64_t* count);
+/* Host-side timing of the last measure call: [0] phase-A enqueue ms, [1]
+ * phase-B enqueue ms, [2] device spin us.  Passing n > 7 with out[7] > 0 sets
+ * the per-call host cost (us) used to size the spin. */
+ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n);
+/* Diagnostics: launch one tcgen05 candidate `launches` times back to back with
+ * per-CTA %globaltimer stamps (8 u64 per CTA: start, setup done, first stage
+ * landed, accumulator done, partial tile staged, stored, smid, 0). */
+ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int launches, uint64_t* out,
+                             int max_ctas, int* n_ctas);
 void ls_runner_destroy(ls_runner* r);
 
 const char* ls_last_error(void);

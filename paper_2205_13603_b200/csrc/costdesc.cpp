@@ -64,29 +64,6 @@ struct Enc {
     return m;
   }
 
-  // one access record into tail; returns false on limits
-  bool access(int buf, const std::vector<Expr*>& idx, int phase, int tile, const std::vector<Stmt*>& enc) {
-    if (idx.size() > static_cast<size_t>(MAX_DIM)) return fail("buffer rank above limit");
-    size_t rec = tail.size();
-    tail.resize(rec + ACC_WORDS, 0);
-    tail[rec + A_BUF] = buf;
-    tail[rec + A_PHASE] = phase;
-    tail[rec + A_NDIM] = static_cast<int64_t>(idx.size());
-    tail[rec + A_TILE] = tile;
-    tail[rec + A_USE] = static_cast<int64_t>(use_mask(idx, enc));
-    for (size_t d = 0; d < idx.size(); ++d) {
-      std::vector<int64_t> ops;
-      if (!code(idx[d], enc, &ops)) return false;
-      if (ops.size() / 2 > 64) return fail("index expression too long");
-      size_t at = tail.size();
-      tail.push_back(static_cast<int64_t>(ops.size() / 2));
-      tail.insert(tail.end(), ops.begin(), ops.end());
-      tail[rec + A_CODE + d] = static_cast<int64_t>(at);
-      tail_tail_fix.push_back(rec + A_CODE + d);
-    }
-    return true;
-  }
-
   // vector-friendliness of this statement for each enclosing position
   uint64_t vf_ok(const Stmt* s, const std::vector<Stmt*>& enc) {
     std::vector<const std::vector<Expr*>*> lists;

@@ -50,8 +50,9 @@ struct TcLaunch {
   int64_t sc_b, sc_m;  // output strides (elements) for batch and M (N contiguous)
   int m, n, k;
   int bn, splits, kt, stages, batch, grid_m, grid_n;
-  int accumulate;      // 1: split-K atomic accumulation into a zeroed C
   int smem_bytes;
+  unsigned long long* trace = nullptr;  // optional per-CTA timeline (8 stamps per CTA)
+  bool pdl = true;                      // programmatic dependent launch
 };
 bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st);
 

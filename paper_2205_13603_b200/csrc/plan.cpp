@@ -237,11 +237,18 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
         if (before_spatial) t.splits *= merged[i].extent;
         else t.kt *= merged[i].extent;
       }
-      plan.needs_zero = t.splits > 1;
+      // split-K above 16 ways cannot form one cluster: fp32 atomics into a zeroed C
+      plan.needs_zero = t.splits > 16;
       int64_t stage = 128 * 64 * 2 + t.bn * 64 * 2;
-      t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, (lim.max_smem - 2048) / stage));
+      // epilogue buffer: cluster split-K receives splits x ceil(128/splits)
+      // padded rows in its own region; otherwise the tile reuses the ring
+      bool cluster = t.splits > 1 && t.splits <= 16;
+      int64_t rows_per = (128 + t.splits - 1) / t.splits;
+      int64_t red = cluster ? t.splits * rows_per * (t.bn + 4) * 4 : 128 * (t.bn + 4) * 4;
+      int64_t avail = lim.max_smem - 2048 - (cluster ? red : 0);
+      t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / stage));
       t.stages = std::min<int64_t>(t.stages, 8);
-      t.smem_bytes = t.stages * stage + 1024 + 256;
+      t.smem_bytes = (cluster ? t.stages * stage + red : std::max(t.stages * stage, red)) + 1024 + 256;
       int32_t* c = plan.cfg;
       c[0] = static_cast<int32_t>(t.batch); c[1] = static_cast<int32_t>(t.grid_m);
       c[2] = static_cast<int32_t>(t.grid_n); c[3] = static_cast<int32_t>(t.bn);

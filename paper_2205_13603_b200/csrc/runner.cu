@@ -102,7 +102,9 @@ struct ls_runner {
   std::vector<cudaEvent_t> ev;             // 4 per candidate slot
   float last_ms = 0.f;
   int64_t launches = 0;
+  double stats[8] = {0};  // host ms phase A, host ms phase B, spin us, phase-B launches
   DeviceLimits lim;
+  double launch_host_us = 4.0;  // host enqueue cost per call, for sizing the device spin
 
   ~ls_runner() { release(); }
 
@@ -151,6 +153,8 @@ struct ls_runner {
   }
 
   // one launch of a planned candidate (plus its zeroing memset)
+  unsigned long long* trace = nullptr;  // set only by ls_runner_trace_tc
+
   bool launch(const Plan& p, bool guarded, int slot) {
     const unsigned long long* dl = guarded ? deadline : nullptr;
     int* flag = flags + slot;
@@ -185,8 +189,8 @@ struct ls_runner {
         L.batch = static_cast<int>(p.tc.batch);
         L.grid_m = static_cast<int>(p.tc.grid_m);
         L.grid_n = static_cast<int>(p.tc.grid_n);
-        L.accumulate = p.tc.splits > 1;
         L.smem_bytes = static_cast<int>(p.tc.smem_bytes);
+        L.trace = trace;
         return launch_tc_gemm(L, st);
       }
       default:
@@ -418,6 +422,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   LSB_CUDA(cudaEventCreate(&batch0));
   LSB_CUDA(cudaEventRecord(batch0, r->st));
 
+  auto host_now = [] { return std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  std::memset(r->stats, 0, sizeof r->stats);
+  double h0 = host_now();
   // ---- phase A: checked run ----
   std::vector<char> launched(static_cast<size_t>(n), 0);
   for (int i = 0; i < n; ++i) {
@@ -467,6 +475,8 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     }
   }
 
+  r->stats[0] = host_now() - h0;
+  h0 = host_now();
   // ---- phase B: timed repeats, chunked behind a device spin ----
   std::vector<int> reps(static_cast<size_t>(n), 0);
   const int chunk = 32;
@@ -485,9 +495,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       gpu_us += rep * wm * 1e3;
     }
     if (!calls) continue;
-    double host_us = 4.0 * static_cast<double>(calls);
+    double host_us = r->launch_host_us * static_cast<double>(calls);
     double spin = host_us - prev_gpu_us;
     if (spin > 0) {
+      r->stats[2] += std::min(spin, 20000.0);
       launch_delay(static_cast<unsigned long long>(std::min(spin, 20000.0) * 1e3), r->st);
       ++r->launches;
     }
@@ -505,6 +516,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     }
     prev_gpu_us = gpu_us;
   }
+  r->stats[1] = host_now() - h0;
   cudaEvent_t batch1;
   LSB_CUDA(cudaEventCreate(&batch1));
   LSB_CUDA(cudaEventRecord(batch1, r->st));
@@ -573,6 +585,57 @@ ls_status ls_runner_launch_count(ls_runner* r, int64_t* count) {
     return LS_ERR_ARG;
   }
   *count = r->launches;
+  return LS_OK;
+}
+
+ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int launches, uint64_t* out,
+                             int max_ctas, int* n_ctas) {
+  if (!r || !r->have_workload || !program || !out || !n_ctas || launches < 1) {
+    set_error("ls_runner_trace_tc: bad arguments");
+    return LS_ERR_ARG;
+  }
+  std::string err;
+  auto p = parse_program(std::string_view(program, len), &err);
+  if (!p) {
+    set_error(err);
+    return LS_ERR_PARSE;
+  }
+  Plan plan = plan_program(r->w, *p, r->lim);
+  if (plan.status != P_OK || plan.family != F_TC) {
+    set_error("ls_runner_trace_tc: program does not instantiate as a tcgen05 candidate");
+    return LS_ERR_ARG;
+  }
+  int ctas = static_cast<int>(plan.tc.grid_m * plan.tc.grid_n * plan.tc.batch * plan.tc.splits);
+  *n_ctas = ctas;
+  LSB_CUDA(cudaSetDevice(r->device));
+  unsigned long long* d = nullptr;
+  LSB_CUDA(cudaMalloc(&d, static_cast<size_t>(ctas) * 8 * 8 * launches));
+  LSB_CUDA(cudaMemsetAsync(d, 0, static_cast<size_t>(ctas) * 8 * 8 * launches, r->st));
+  bool ok = true;
+  for (int i = 0; i < launches && ok; ++i) {
+    r->trace = d + static_cast<size_t>(i) * ctas * 8;
+    ok = r->launch(plan, false, 0);
+  }
+  r->trace = nullptr;
+  cudaError_t e = cudaStreamSynchronize(r->st);
+  int keep = std::min(max_ctas, ctas * launches);
+  if (ok && e == cudaSuccess)
+    e = cudaMemcpy(out, d, static_cast<size_t>(keep) * 8 * 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (!ok || e != cudaSuccess) {
+    set_error("ls_runner_trace_tc: launch failed");
+    return LS_ERR_CUDA;
+  }
+  return LS_OK;
+}
+
+ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n) {
+  if (!r || !out) {
+    set_error("ls_runner_debug_stats: bad arguments");
+    return LS_ERR_ARG;
+  }
+  for (int i = 0; i < n && i < 8; ++i) out[i] = r->stats[i];
+  if (n > 7 && out[7] > 0) r->launch_host_us = out[7];  // optional override (us per call)
   return LS_OK;
 }
 

@@ -4,8 +4,17 @@
 // Warp roles (128 threads):
 //   warp 0  : TMEM allocation; lane 0 is the TMA producer
 //   warp 1  : lane 0 initialises the mbarriers and issues tcgen05.mma
+// Launched with programmatic dependent launch: setup (TMEM allocation,
+// barrier init, descriptor prefetch) overlaps the previous grid's tail and
+// griddepcontrol.wait guards every global access.
 //   warps 0-3: epilogue -- tcgen05.ld of their 32 TMEM lanes (= 32 output
-//             rows), then plain stores (split-K: fp32 red.global.add).
+//             rows) into a shared-memory tile, then coalesced row-segment
+//             stores.
+// Split-K: the split CTAs of one output tile form a thread-block cluster
+// (cluster dims 1 x 1 x splits, <= 16) and reduce their partial tiles through
+// distributed shared memory -- each CTA sums one slice of rows across all
+// peers (ld.shared::cluster) and writes it once.  No memset, no atomics.
+// Above 16 ways the tile falls back to fp32 red.global.add into a zeroed C.
 // The k loop is an S-stage smem ring: full[s] (TMA tx-count) and empty[s]
 // (tcgen05.commit) mbarriers.  Instantiated at runtime for any BN in
 // [16, 256] step 16, split-K ways, k-tiles and stage count (see plan.cpp).
@@ -22,7 +31,9 @@ namespace {
 struct TcArgs {
   float* c;
   int64_t sc_b, sc_m;
-  int bn, splits, kt, stages, accumulate;
+  int bn, splits, kt, stages;
+  int mode;  // 0 single CTA per tile, 1 cluster DSMEM reduction, 2 atomic accumulation
+  unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA)
   uint32_t idesc;
   uint32_t tmem_cols;
 };
@@ -102,7 +113,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+
+__device__ __forceinline__ void st_cluster_f4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 constexpr int kTile = 128 * 64 * 2;  // A stage bytes
+constexpr int kMaxClusterSplits = 16;
 
 __global__ void __launch_bounds__(128, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, TcArgs a) {
@@ -113,12 +150,26 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   const int b_bytes = a.bn * 64 * 2;
   const uint32_t a0 = base;                                  // A stages
   const uint32_t b0 = base + a.stages * kTile;               // B stages
-  const uint32_t bars = b0 + a.stages * b_bytes;             // full[S], empty[S], done
+  const int red_ld = a.bn + 4;                               // padded row (floats)
+  const uint32_t stage_end = b0 + a.stages * b_bytes;
+  // epilogue buffer: cluster mode receives every peer's rows of this CTA's
+  // slice in a region of its own (peers may push while we still run the
+  // main loop); single-CTA modes stage their own tile over the finished ring
+  const int S_cl = a.mode == 1 ? a.splits : 1;
+  const int rows_per = (128 + S_cl - 1) / S_cl;
+  const uint32_t red = a.mode == 1 ? ((stage_end + 15u) & ~15u) : base;
+  const uint32_t red_bytes = a.mode == 1 ? static_cast<uint32_t>(S_cl * rows_per * red_ld * 4)
+                                         : static_cast<uint32_t>(128 * red_ld * 4);
+  const uint32_t red_end = red + red_bytes;
+  const uint32_t bars = ((stage_end > red_end ? stage_end : red_end) + 15u) & ~15u;
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_blk = blockIdx.x, m_blk = blockIdx.y;
+  const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtime();
   const int batch = blockIdx.z / a.splits, split = blockIdx.z % a.splits;
 
   if (warp == 0) {
@@ -141,6 +192,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
+
+  // programmatic dependent launch: the next grid may start its prologue now;
+  // this grid waits for its predecessor before its first global access
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -161,6 +218,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
       const uint32_t ph = (kt / a.stages) & 1;
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
+      if (tr && kt == 0) tr[2] = gtime();
       const uint32_t sa = a0 + s * kTile, sb = b0 + s * b_bytes;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
@@ -170,23 +228,70 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
     umma_commit(done);
   }
 
-  // ---- epilogue: TMEM -> registers -> global ----
+  // ---- epilogue ----
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
-  const int row = m_blk * 128 + warp * 32 + lane;
-  float* crow = a.c + batch * a.sc_b + static_cast<int64_t>(row) * a.sc_m + static_cast<int64_t>(n_blk) * a.bn;
-  for (int c0 = 0; c0 < a.bn; c0 += 16) {
-    float v[16];
-    tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-    float4* dst = reinterpret_cast<float4*>(crow + c0);
-    if (a.accumulate) {
+  if (tr && threadIdx.x == 0) tr[3] = gtime();
+  const int row = warp * 32 + lane;  // TMEM lane == output row of this thread
+  const int c4 = a.bn / 4;
+  float* ctile = a.c + batch * a.sc_b + static_cast<int64_t>(m_blk) * 128 * a.sc_m + static_cast<int64_t>(n_blk) * a.bn;
+  if (a.mode == 1) {
+    // push: row -> the peer that owns its slice, straight from registers
+    const uint32_t me = cluster_rank();
+    const int owner = row / rows_per, lr = row - owner * rows_per;
+    const uint32_t dst =
+        map_peer(red + static_cast<uint32_t>(((static_cast<int>(me) * rows_per + lr) * red_ld) * 4), owner);
+    for (int c0 = 0; c0 < a.bn; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) atomicAdd(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      for (int q = 0; q < 4; ++q)
+        st_cluster_f4(dst + static_cast<uint32_t>((c0 + 4 * q) * 4), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
+    cluster_sync_all();  // every pushed row has landed
+    if (tr && threadIdx.x == 0) tr[4] = gtime();
+    const int r_lo = static_cast<int>(me) * rows_per;
+    const int nrows = min(128, r_lo + rows_per) - r_lo;
+    const float* rb = reinterpret_cast<const float*>(gbase + (red - base));
+    for (int e = threadIdx.x; e < nrows * c4; e += 128) {
+      const int lr2 = e / c4, cc = (e % c4) * 4;
+      float4 v[kMaxClusterSplits];
+#pragma unroll
+      for (int q = 0; q < kMaxClusterSplits; ++q)
+        if (q < S_cl) v[q] = *reinterpret_cast<const float4*>(rb + (q * rows_per + lr2) * red_ld + cc);
+      float4 acc = v[0];
+#pragma unroll
+      for (int q = 1; q < kMaxClusterSplits; ++q)
+        if (q < S_cl) { acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w; }
+      *reinterpret_cast<float4*>(ctile + static_cast<int64_t>(r_lo + lr2) * a.sc_m + cc) = acc;
+    }
+  } else {
+    // stage the tile over the finished smem ring, then coalesced row segments
+    float* stg = reinterpret_cast<float*>(gbase) + row * red_ld;
+    for (int c0 = 0; c0 < a.bn; c0 += 16) {
+      float v[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(stg + c0 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[4] = gtime();
+    const float* sb = reinterpret_cast<const float*>(gbase);
+    for (int e = threadIdx.x; e < 128 * c4; e += 128) {
+      const int r = e / c4, cc = (e % c4) * 4;
+      const float4 acc = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
+      float4* dst = reinterpret_cast<float4*>(ctile + static_cast<int64_t>(r) * a.sc_m + cc);
+      if (a.mode == 2) atomicAdd(dst, acc);
+      else *dst = acc;
+    }
+  }
+  if (tr && threadIdx.x == 0) {
+    tr[5] = gtime();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[6] = smid;
   }
   tc_fence_before();
   __syncthreads();
@@ -209,17 +314,43 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.splits = L.splits;
   a.kt = L.kt;
   a.stages = L.stages;
-  a.accumulate = L.accumulate;
+  a.mode = L.splits == 1 ? 0 : (L.splits <= kMaxClusterSplits ? 1 : 2);
+  a.trace = L.trace;
   // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N>>3, M>>4
   a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(L.bn >> 3) << 17) |
             (static_cast<uint32_t>(128 >> 4) << 24);
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(L.bn)) cols <<= 1;
   a.tmem_cols = cols;
-  dim3 grid(static_cast<unsigned>(L.grid_n), static_cast<unsigned>(L.grid_m),
-            static_cast<unsigned>(L.batch * L.splits));
-  tc_gemm_kernel<<<grid, 128, L.smem_bytes, st>>>(*static_cast<const CUtensorMap*>(L.tmap_a),
-                                                  *static_cast<const CUtensorMap*>(L.tmap_b), a);
+  static bool nonportable = false;
+  if (a.mode == 1 && L.splits > 8 && !nonportable) {
+    if (cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    nonportable = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(L.grid_n), static_cast<unsigned>(L.grid_m),
+                     static_cast<unsigned>(L.batch * L.splits));
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = static_cast<size_t>(L.smem_bytes);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = a.mode == 1 ? static_cast<unsigned>(L.splits) : 1u;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = L.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const CUtensorMap ta = *static_cast<const CUtensorMap*>(L.tmap_a);
+  const CUtensorMap tb = *static_cast<const CUtensorMap*>(L.tmap_b);
+  if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ta, tb, a) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
   return cudaGetLastError() == cudaSuccess;
 }
 

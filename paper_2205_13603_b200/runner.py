@@ -151,6 +151,13 @@ class B200Runner:
         native.check(native.lib().ls_runner_launch_count(self._h, ctypes.byref(v)), "launches")
         return int(v.value)
 
+    def debug_stats(self, launch_host_us: float = 0.0) -> dict:
+        a = np.zeros(8, np.float64)
+        a[7] = launch_host_us
+        native.check(native.lib().ls_runner_debug_stats(self._h, native.as_np_ptr(a, ctypes.c_double), 8),
+                     "debug_stats")
+        return {"phase_a_host_ms": a[0], "phase_b_host_ms": a[1], "spin_us": a[2]}
+
     def last_output(self) -> np.ndarray:
         import json
         doc = json.loads(self.e0_json)

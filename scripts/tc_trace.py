@@ -1,0 +1,36 @@
+"""Per-CTA timeline of a tcgen05 candidate (globaltimer stamps)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from conftest import load_population  # noqa: E402
+from paper_2205_13603_b200 import native  # noqa: E402
+from paper_2205_13603_b200.runner import B200Runner  # noqa: E402
+
+want = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,1,12,64,12").split(",")]
+launches = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+hdr, pop = load_population("bert_ffn")
+r = B200Runner(dtype="bf16")
+r.set_workload(hdr["e0"])
+progs = [p["program"] for p in pop]
+plans = r.plan_programs(progs)
+i = next(i for i, p in enumerate(plans) if p["family"] == "tcgen05" and p["cfg"][:len(want)] == want)
+print("cfg", plans[i]["cfg"][:8])
+b = progs[i].encode()
+buf = (ctypes.c_uint64 * (8 * 4096))()
+n = ctypes.c_int()
+native.check(native.lib().ls_runner_trace_tc(r._h, b, len(b), launches, buf, 4096 // 1, ctypes.byref(n)), "trace")
+a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8)[: n.value * launches].astype(np.int64)
+t0 = a[:, 0].min()
+for L in range(launches):
+    s = a[L * n.value:(L + 1) * n.value]
+    rel = (s[:, :6] - t0) / 1000.0
+    print(f"launch {L}: start [{rel[:,0].min():.2f},{rel[:,0].max():.2f}] setup+{np.median(rel[:,1]-rel[:,0]):.2f} "
+          f"firstload+{np.median(rel[:,2]-rel[:,1]):.2f} mma_done+{np.median(rel[:,3]-rel[:,2]):.2f} "
+          f"staged+{np.median(rel[:,4]-rel[:,3]):.2f} stored+{np.median(rel[:,5]-rel[:,4]):.2f} "
+          f"end [{rel[:,5].min():.2f},{rel[:,5].max():.2f}] us")
