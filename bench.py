@@ -202,7 +202,8 @@ def run_b200(args):
     probe.close()
     timeout_ms = max(0.05, 2.0 * base["latency_ns"] / 1e6)
     runner = B200Runner(device=local, dtype=dtype, min_repeats=3, max_repeats=50, target_ms=0.02,
-                        timeout_ms=timeout_ms)
+                        timeout_ms=timeout_ms, timeout_factor=args.timeout_factor,
+                        timeout_floor_ms=0.05)
     scorer = GpuScorer(local)
     devbatch = DeviceBatch(texts, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -267,7 +268,8 @@ def run_b200(args):
                        "candidates_per_rank_per_step": len(texts), "input_seed": 0,
                        "l2": "flushed (256 MB scrub) between steps; candidate repeats run L2-warm",
                        "runner": {"min_repeats": 3, "max_repeats": 50, "target_ms": 0.02,
-                                  "timeout_ms": round(timeout_ms, 4), "parity": "exact (integer inputs)"}},
+                                  "timeout_cap_ms": round(timeout_ms, 4), "timeout_factor": args.timeout_factor,
+                                  "timeout_floor_ms": 0.05, "parity": "exact (integer inputs)"}},
             "e2e": {"value": total_cands / wall_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -302,6 +304,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
     ap.add_argument("--cpu-budget", type=float, default=8.0)
+    ap.add_argument("--timeout-factor", type=float, default=20.0,
+                    help="checked launches get clamp(factor x best-so-far, 0.05 ms, 2 x e0) before abort")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

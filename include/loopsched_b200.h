@@ -90,10 +90,12 @@ typedef struct {
   int32_t min_repeats;     /* timed launches per candidate (lower bound)          */
   int32_t max_repeats;     /* upper bound                                          */
   double target_ms;        /* repeats sized so one candidate runs ~target_ms       */
-  double timeout_ms;       /* device-side deadline for the first launch            */
+  double timeout_ms;       /* device-side deadline cap for the checked launch      */
   double rtol, atol;       /* parity tolerance against the e0 reference output     */
-  int32_t flush_l2;        /* 1: scrub L2 before every timed launch                */
-  int32_t reserved[7];
+  int32_t flush_l2;        /* reserved (must be 0)                                 */
+  int32_t reserved0;
+  double timeout_factor;   /* >0: deadline = clamp(factor x best-so-far, floor,   */
+  double timeout_floor_ms; /*      timeout_ms), tracked on the device              */
 } ls_runner_opts;
 
 /* per-candidate status */
@@ -104,7 +106,8 @@ enum {
   LS_RUN_PARSE = 3,
   LS_RUN_LAUNCH = 4,
   LS_RUN_PARITY = 5,       /* output differs from the reference output           */
-  LS_RUN_TIMEOUT = 6       /* first launch exceeded timeout_ms                   */
+  LS_RUN_TIMEOUT = 6       /* checked launch passed its deadline; latency_ns is  */
+                           /* the abort time, a lower bound                      */
 };
 
 /* kernel families */

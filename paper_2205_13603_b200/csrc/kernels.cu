@@ -163,8 +163,8 @@ __global__ void loopnest_contract(const T* __restrict__ x, const T* __restrict__
 }
 
 // ---- K6 parity reducer -------------------------------------------------------
-__global__ void parity_kernel(const float* __restrict__ c, const double* __restrict__ ref, int64_t n, double rtol,
-                              double atol, unsigned long long* slot) {
+__global__ void parity_kernel(float* __restrict__ c, const double* __restrict__ ref, int64_t n, double rtol,
+                              double atol, unsigned long long* slot, int poison) {
   double worst = 0.0;
   unsigned long long bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -173,6 +173,7 @@ __global__ void parity_kernel(const float* __restrict__ c, const double* __restr
     if (!(err <= atol + rtol * fabs(r))) ++bad;
     if (isnan(err)) err = INFINITY;
     worst = fmax(worst, err);
+    if (poison) c[i] = __int_as_float(0x7fffffff);
   }
   for (int o = 16; o; o >>= 1) {
     worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
@@ -184,7 +185,21 @@ __global__ void parity_kernel(const float* __restrict__ c, const double* __restr
   }
 }
 
-__global__ void set_deadline_kernel(unsigned long long* d, unsigned long long ns) { *d = gtimer() + ns; }
+__global__ void arm_kernel(unsigned long long* s, const int* prev_flag, const unsigned long long* prev_parity,
+                           double factor, unsigned long long floor_ns, unsigned long long cap_ns) {
+  const unsigned long long now = gtimer();
+  if (prev_flag && !*prev_flag && prev_parity[1] == 0) {
+    unsigned long long el = now - s[1];
+    if (el < s[2]) s[2] = el;
+  }
+  unsigned long long t = cap_ns;
+  if (factor > 0.0 && s[2] != ~0ull) {
+    double want = factor * (double)s[2];
+    t = want < (double)floor_ns ? floor_ns : (want > (double)cap_ns ? cap_ns : (unsigned long long)want);
+  }
+  s[0] = now + t;
+  s[1] = now;
+}
 
 __global__ void delay_kernel(unsigned long long ns) {
   unsigned long long end = gtimer() + ns;
@@ -347,13 +362,14 @@ void launch_loopnest(const void* x, const void* y, float* c, const LoopNestCfg& 
     loopnest_contract<float><<<g, threads, 0, st>>>(static_cast<const float*>(x), static_cast<const float*>(y), c, a);
 }
 
-void launch_parity(const float* c, const double* ref, int64_t n, double rtol, double atol, unsigned long long* slot,
-                   cudaStream_t st) {
-  parity_kernel<<<grid_for(n, 256), 256, 0, st>>>(c, ref, n, rtol, atol, slot);
+void launch_parity(float* c, const double* ref, int64_t n, double rtol, double atol, unsigned long long* slot,
+                   bool poison, cudaStream_t st) {
+  parity_kernel<<<grid_for(n, 256), 256, 0, st>>>(c, ref, n, rtol, atol, slot, poison ? 1 : 0);
 }
 
-void launch_set_deadline(unsigned long long* d, unsigned long long ns, cudaStream_t st) {
-  set_deadline_kernel<<<1, 1, 0, st>>>(d, ns);
+void launch_arm(unsigned long long* state, const int* prev_flag, const unsigned long long* prev_parity,
+                double factor, unsigned long long floor_ns, unsigned long long cap_ns, cudaStream_t st) {
+  arm_kernel<<<1, 1, 0, st>>>(state, prev_flag, prev_parity, factor, floor_ns, cap_ns);
 }
 
 void launch_delay(unsigned long long ns, cudaStream_t st) { delay_kernel<<<1, 1, 0, st>>>(ns); }

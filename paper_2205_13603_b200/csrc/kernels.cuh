@@ -26,11 +26,17 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
 // LOOPNEST family.
 void launch_loopnest(const void* x, const void* y, float* c, const LoopNestCfg& cfg, bool bf16,
                      const unsigned long long* deadline, int* timed_out, cudaStream_t st);
-// K6 parity reducer: slot[0] = max |c - ref| (as double bits), slot[1] = mismatches.
-void launch_parity(const float* c, const double* ref, int64_t n, double rtol, double atol,
-                   unsigned long long* slot, cudaStream_t st);
-// deadline = globaltimer + ns (device side, right before the guarded launch)
-void launch_set_deadline(unsigned long long* deadline, unsigned long long ns, cudaStream_t st);
+// K6 parity reducer: slot[0] = max |c - ref| (as double bits), slot[1] =
+// mismatches; with poison, every checked element is then overwritten with NaN
+// so a later candidate that skips an element fails its own check.
+void launch_parity(float* c, const double* ref, int64_t n, double rtol, double atol, unsigned long long* slot,
+                   bool poison, cudaStream_t st);
+// Device-side deadline state: [0] deadline, [1] arm time, [2] best elapsed ns.
+// arm: first settles the previous candidate (its elapsed time updates best
+// when it neither timed out nor failed parity), then sets deadline = now +
+// clamp(factor * best, floor, cap) (cap while nothing has succeeded yet).
+void launch_arm(unsigned long long* state, const int* prev_flag, const unsigned long long* prev_parity,
+                double factor, unsigned long long floor_ns, unsigned long long cap_ns, cudaStream_t st);
 // spin on the device for ~ns (lets the host queue a chunk of launches)
 void launch_delay(unsigned long long ns, cudaStream_t st);
 // fp32 -> bf16 copy, and an optional 2-D transpose to make K contiguous

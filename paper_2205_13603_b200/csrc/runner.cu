@@ -95,7 +95,7 @@ struct ls_runner {
   Strides s{};
   CUtensorMap tmap_a{};
   std::map<int, CUtensorMap> tmap_b;
-  unsigned long long* deadline = nullptr;  // [0] armed deadline
+  unsigned long long* deadline = nullptr;  // device deadline state: [0] deadline, [1] arm time, [2] best ns
   int* flags = nullptr;                    // per-candidate timeout flags
   unsigned long long* parity = nullptr;    // per-candidate (max err bits, mismatches)
   int cap = 0;
@@ -279,6 +279,8 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   o.timeout_ms = 2.0;
   o.rtol = 0.0;
   o.atol = 0.0;
+  o.timeout_factor = 0.0;
+  o.timeout_floor_ms = 0.05;
   if (opts) o = *opts;
   if (o.min_repeats < 1) o.min_repeats = 1;
   if (o.max_repeats < o.min_repeats) o.max_repeats = o.min_repeats;
@@ -287,7 +289,7 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   r->lim.max_threads = prop.maxThreadsPerBlock;
   r->lim.max_smem = static_cast<int64_t>(prop.sharedMemPerBlockOptin) - 1024;
   LSB_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
-  LSB_CUDA(cudaMalloc(&r->deadline, 2 * sizeof(unsigned long long)));
+  LSB_CUDA(cudaMalloc(&r->deadline, 4 * sizeof(unsigned long long)));
   ls_status s = r->ensure_capacity(256);
   if (s != LS_OK) return s;
   *out = r.release();
@@ -427,12 +429,29 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   std::memset(r->stats, 0, sizeof r->stats);
   double h0 = host_now();
   // ---- phase A: checked run ----
+  // C starts poisoned (NaN) and the parity reducer re-poisons it, so any
+  // element a candidate fails to write is a mismatch.  The deadline of each
+  // checked launch is armed on the device from the best time seen so far.
   std::vector<char> launched(static_cast<size_t>(n), 0);
-  for (int i = 0; i < n; ++i) {
+  const unsigned long long best_init[3] = {0, 0, ~0ull};
+  LSB_CUDA(cudaMemcpyAsync(r->deadline, best_init, sizeof best_init, cudaMemcpyHostToDevice, r->st));
+  LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
+  const unsigned long long floor_ns = static_cast<unsigned long long>(r->opts.timeout_floor_ms * 1e6);
+  // checked-run order: families expected to be fast first, so the device-side
+  // best-so-far (and with it every later deadline) drops early; results are
+  // still reported in candidate order
+  std::vector<int> order;
+  for (int pass = 0; pass < 4; ++pass) {
+    static const int fam_order[4] = {F_TC, F_SIMT, F_NAIVE, F_LOOPNEST};
+    for (int i = 0; i < n; ++i)
+      if (plans[static_cast<size_t>(i)].status == P_OK && plans[static_cast<size_t>(i)].family == fam_order[pass])
+        order.push_back(i);
+  }
+  int prev = -1;
+  for (int i : order) {
     const Plan& p = plans[static_cast<size_t>(i)];
-    if (p.status != P_OK) continue;
-    LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));  // NaN poison: unwritten outputs fail parity
-    launch_set_deadline(r->deadline, timeout_ns, r->st);
+    launch_arm(r->deadline, prev >= 0 ? r->flags + prev : nullptr, prev >= 0 ? r->parity + 2 * prev : nullptr,
+               r->opts.timeout_factor, floor_ns, timeout_ns, r->st);
     ++r->launches;
     LSB_CUDA(cudaEventRecord(E[4 * i], r->st));
     bool ok = r->launch(p, true, i);
@@ -440,11 +459,13 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     if (!ok) {
       cudaGetLastError();
       out[i].status = LS_RUN_LAUNCH;
+      LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
       continue;
     }
-    launch_parity(r->c, r->ref, r->w.c_elems, r->opts.rtol, r->opts.atol, r->parity + 2 * i, r->st);
+    launch_parity(r->c, r->ref, r->w.c_elems, r->opts.rtol, r->opts.atol, r->parity + 2 * i, true, r->st);
     ++r->launches;
     launched[static_cast<size_t>(i)] = 1;
+    prev = i;
   }
   cudaError_t se = cudaStreamSynchronize(r->st);
   if (se != cudaSuccess) {
@@ -467,7 +488,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     out[i].mismatches = static_cast<int64_t>(par[static_cast<size_t>(2 * i + 1)]);
     if (tflag[static_cast<size_t>(i)]) {
       out[i].status = LS_RUN_TIMEOUT;
-      out[i].latency_ns = r->opts.timeout_ms * 1e6;
+      out[i].latency_ns = 1e6 * static_cast<double>(warm[static_cast<size_t>(i)]);  // abort time: lower bound
       out[i].repeats = 1;
       launched[static_cast<size_t>(i)] = 0;
     } else if (out[i].mismatches) {

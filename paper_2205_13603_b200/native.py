@@ -42,7 +42,8 @@ class RunnerOptsC(ctypes.Structure):
                 ("max_repeats", ctypes.c_int32), ("target_ms", ctypes.c_double),
                 ("timeout_ms", ctypes.c_double), ("rtol", ctypes.c_double),
                 ("atol", ctypes.c_double), ("flush_l2", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 7)]
+                ("reserved0", ctypes.c_int32), ("timeout_factor", ctypes.c_double),
+                ("timeout_floor_ms", ctypes.c_double)]
 
 
 class ResultC(ctypes.Structure):

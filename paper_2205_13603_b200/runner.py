@@ -43,13 +43,15 @@ class B200Runner:
 
     def __init__(self, device: int = 0, dtype: str = "bf16", min_repeats: int = 3,
                  max_repeats: int = 200, target_ms: float = 0.2, timeout_ms: float = 2.0,
-                 rtol: float = 0.0, atol: float = 0.0, sentinel_factor: float = 1e4):
+                 rtol: float = 0.0, atol: float = 0.0, sentinel_factor: float = 1e4,
+                 timeout_factor: float = 0.0, timeout_floor_ms: float = 0.05):
         L = native.lib()
         o = native.RunnerOptsC()
         o.dtype = 1 if dtype == "bf16" else 0
         o.min_repeats, o.max_repeats = min_repeats, max_repeats
         o.target_ms, o.timeout_ms = target_ms, timeout_ms
         o.rtol, o.atol = rtol, atol
+        o.timeout_factor, o.timeout_floor_ms = timeout_factor, timeout_floor_ms
         h = ctypes.c_void_p()
         native.check(L.ls_runner_create(device, ctypes.byref(o), ctypes.byref(h)),
                      "ls_runner_create")
@@ -129,10 +131,14 @@ class B200Runner:
         return self.baseline() * Fraction(self.sentinel_factor)
 
     def latencies(self, results) -> list:
+        """OK -> measured ns; TIMEOUT -> the abort time (a lower bound, still
+        ordered below every failure); anything else -> the finite sentinel."""
         out = []
         for r in results:
             if r["status"] == "OK":
                 out.append(ns_fraction(r["latency_ns"]))
+            elif r["status"] == "TIMEOUT" and r["latency_ns"] > 0:
+                out.append(min(ns_fraction(r["latency_ns"]), self.sentinel()))
             else:
                 out.append(self.sentinel())
         return out

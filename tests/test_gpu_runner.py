@@ -119,7 +119,33 @@ def test_statuses_and_sentinels():
     assert res[-1]["status"] == "PARSE"
     lats = r.latencies(res)
     base = r.baseline()
-    assert all(l == base * 10 ** 4 for l in lats)  # finite sentinel, never inf
+    sentinel = base * 10 ** 4  # finite, never inf (fit takes log latency)
+    assert all(l == sentinel for l, x in zip(lats, res) if x["status"] != "TIMEOUT")
+    for l, x in zip(lats, res):
+        if x["status"] == "TIMEOUT":  # abort time: a lower bound above the deadline
+            assert 0.05e6 <= float(l) <= float(sentinel)
+    r.close()
+
+
+def test_adaptive_timeout_bounds_slow_candidates():
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    r = make_runner("bf16", timeout_ms=5.0, timeout_factor=10.0, timeout_floor_ms=0.02)
+    r.set_workload(e0, seed=0)
+    progs = [p["program"] for p in pop[:300]]
+    plans = r.plan_programs(progs)
+    fast = pick(plans, "tcgen05", 2)
+    slow = pick(plans, "simt", 40)
+    res = r.measure_programs([progs[i] for i in fast + slow])
+    best = min(x["latency_ns"] for x in res if x["status"] == "OK")
+    for x in res[len(fast):]:
+        if x["status"] == "OK":
+            assert x["mismatches"] == 0
+        else:
+            assert x["status"] == "TIMEOUT"
+            # aborted near 10x the best checked run seen before it, far below the 5 ms cap
+            assert x["latency_ns"] < 2.5e6
+    assert any(x["status"] == "TIMEOUT" for x in res)
     r.close()
 
 
