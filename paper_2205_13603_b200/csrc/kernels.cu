@@ -25,6 +25,10 @@ struct SArgs {
   Strides s;
   int64_t tb, tm, tn, rb, bk, kt;
   int x_kfast, y_kfast;
+  int va, vb;                 // global vector width (1 or 16 bytes' worth) per operand
+  int lda, ldb;               // padded smem row lengths
+  int a_vec_smem, b_vec_smem; // 128-bit smem reads possible
+  int c_vec;                  // 128-bit output stores possible
   const unsigned long long* deadline;
   int* timed_out;
 };
@@ -49,23 +53,88 @@ __global__ void contract_naive(const T* __restrict__ x, const T* __restrict__ y,
 // CTA (gn, gm, gb) owns a BM x BN output tile of tb*rb batches; thread
 // (tb_i, tm_i, tn_i) owns an RM x RN register tile (rows tm_i*RM.., cols
 // tn_i*RN..) of rb batches; k runs in kt shared-memory tiles of bk.
+// Tiles are staged k-major in shared memory (S[tb][kk][row], rows padded when
+// that breaks bank conflicts); global loads walk the operand's contiguous
+// dimension with 16-byte vectors when the tile and strides allow it and use
+// carried indices instead of per-element division.
+template <typename T> struct VecW { static constexpr int v = 4; };
+template <> struct VecW<__nv_bfloat16> { static constexpr int v = 8; };
+
+template <typename T, int V>
+__device__ __forceinline__ void ld_vec(const T* p, float* out) {
+  if constexpr (V == 1) {
+    out[0] = ldf(p, 0);
+  } else if constexpr (sizeof(T) == 4) {
+    float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    out[0] = q.x; out[1] = q.y; out[2] = q.z; out[3] = q.w;
+  } else {
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      out[2 * i] = f.x; out[2 * i + 1] = f.y;
+    }
+  }
+}
+
+// Stage one operand tile S[t][kk][r] (t < nt, kk < bk, r < nr) from global
+// g[b*s_b + (r0+r)*s_r + (k0+kk)*s_k].  kfast: k is the vector/contiguous
+// dimension, else r is.
+template <typename T, int V>
+__device__ __forceinline__ void stage_tile(float* S, int lds, const T* __restrict__ g, int64_t s_b, int64_t s_r,
+                                           int64_t s_k, int64_t b0, int64_t brb, int64_t rbi, int64_t r0, int64_t k0,
+                                           int nt, int nr, int bk, bool kfast, int tid, int nthr) {
+  const int nf = (kfast ? bk : nr) / V;   // vectors along the fast dim
+  const int ns = kfast ? nr : bk;          // slow dim
+  const int total = nt * ns * nf;
+  if (tid >= total) return;
+  int f = tid % nf, q = tid / nf, sl = q % ns, t = q / ns;
+  const int sf = nthr % nf, sq = nthr / nf, ss = sq % ns, st = sq / ns;
+  for (int e = tid; e < total; e += nthr) {
+    const int64_t b = b0 + t * brb + rbi;
+    float v[V];
+    if (kfast) {
+      const int kk = f * V, r = sl;
+      ld_vec<T, V>(g + b * s_b + (r0 + r) * s_r + (k0 + kk) * s_k, v);
+      float* d = S + (t * bk + kk) * lds + r;
+#pragma unroll
+      for (int i = 0; i < V; ++i) d[i * lds] = v[i];
+    } else {
+      const int r = f * V, kk = sl;
+      ld_vec<T, V>(g + b * s_b + (r0 + r) * s_r + (k0 + kk) * s_k, v);
+      float* d = S + (t * bk + kk) * lds + r;
+#pragma unroll
+      for (int i = 0; i < V; ++i) d[i] = v[i];
+    }
+    f += sf;
+    int c = 0;
+    if (f >= nf) { f -= nf; c = 1; }
+    sl += ss + c;
+    c = 0;
+    if (sl >= ns) { sl -= ns; c = 1; }
+    t += st + c;
+  }
+}
+
 template <typename T, int RM, int RN>
 __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const T* __restrict__ y,
                                                   float* __restrict__ c, SArgs a) {
   extern __shared__ float sm[];
   __shared__ int abort_flag;
+  constexpr int VW = VecW<T>::v;
   const int tid = threadIdx.x;
   const int nthr = (int)(a.tb * a.tm * a.tn);
   const int tn_i = tid % (int)a.tn;
   const int tm_i = (tid / (int)a.tn) % (int)a.tm;
   const int tb_i = tid / (int)(a.tn * a.tm);
   const int bm = (int)a.tm * RM, bn = (int)a.tn * RN, bk = (int)a.bk;
+  const int lda = a.lda, ldb = a.ldb;
   float* As = sm;
-  float* Bs = sm + a.tb * bk * bm;
+  float* Bs = sm + ((a.tb * bk * lda + 3) & ~(int64_t)3);  // 16-byte aligned B tile
   const int64_t m0 = (int64_t)blockIdx.y * bm, n0 = (int64_t)blockIdx.x * bn;
   const int64_t b0 = (int64_t)blockIdx.z * a.tb * a.rb;
   const Strides& s = a.s;
-  const int a_total = (int)a.tb * bm * bk, b_total = (int)a.tb * bn * bk;
 
   for (int64_t rbi = 0; rbi < a.rb; ++rbi) {
     float acc[RM][RN];
@@ -84,29 +153,54 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
         }
       }
       const int64_t k0 = kti * bk;
-      for (int e = tid; e < a_total; e += nthr) {
-        int kk, mm, tbx;
-        if (a.x_kfast) { kk = e % bk; int r = e / bk; mm = r % bm; tbx = r / bm; }
-        else { mm = e % bm; int r = e / bm; kk = r % bk; tbx = r / bk; }
-        const int64_t b = b0 + tbx * a.rb + rbi;
-        As[(tbx * bk + kk) * bm + mm] = ldf(x, b * s.sx[0] + (m0 + mm) * s.sx[1] + (k0 + kk) * s.sx[3]);
-      }
-      for (int e = tid; e < b_total; e += nthr) {
-        int kk, nn, tbx;
-        if (a.y_kfast) { kk = e % bk; int r = e / bk; nn = r % bn; tbx = r / bn; }
-        else { nn = e % bn; int r = e / bn; kk = r % bk; tbx = r / bk; }
-        const int64_t b = b0 + tbx * a.rb + rbi;
-        Bs[(tbx * bk + kk) * bn + nn] = ldf(y, b * s.sy[0] + (n0 + nn) * s.sy[2] + (k0 + kk) * s.sy[3]);
-      }
+      if (a.va > 1)
+        stage_tile<T, VW>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk, a.x_kfast,
+                          tid, nthr);
+      else
+        stage_tile<T, 1>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk, a.x_kfast,
+                         tid, nthr);
+      if (a.vb > 1)
+        stage_tile<T, VW>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk, a.y_kfast,
+                          tid, nthr);
+      else
+        stage_tile<T, 1>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk, a.y_kfast,
+                         tid, nthr);
       __syncthreads();
-      const float* Ap = As + (int64_t)tb_i * bk * bm + tm_i * RM;
-      const float* Bp = Bs + (int64_t)tb_i * bk * bn + tn_i * RN;
+      const float* Ap = As + (int64_t)tb_i * bk * lda + tm_i * RM;
+      const float* Bp = Bs + (int64_t)tb_i * bk * ldb + tn_i * RN;
+#pragma unroll 4
       for (int kk = 0; kk < bk; ++kk) {
         float av[RM], bv[RN];
+        if constexpr (RM % 4 == 0) {
+          if (a.a_vec_smem) {
 #pragma unroll
-        for (int i = 0; i < RM; ++i) av[i] = Ap[kk * bm + i];
+            for (int i = 0; i < RM; i += 4) {
+              float4 q = *reinterpret_cast<const float4*>(Ap + kk * lda + i);
+              av[i] = q.x; av[i + 1] = q.y; av[i + 2] = q.z; av[i + 3] = q.w;
+            }
+          } else {
 #pragma unroll
-        for (int j = 0; j < RN; ++j) bv[j] = Bp[kk * bn + j];
+            for (int i = 0; i < RM; ++i) av[i] = Ap[kk * lda + i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < RM; ++i) av[i] = Ap[kk * lda + i];
+        }
+        if constexpr (RN % 4 == 0) {
+          if (a.b_vec_smem) {
+#pragma unroll
+            for (int j = 0; j < RN; j += 4) {
+              float4 q = *reinterpret_cast<const float4*>(Bp + kk * ldb + j);
+              bv[j] = q.x; bv[j + 1] = q.y; bv[j + 2] = q.z; bv[j + 3] = q.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < RN; ++j) bv[j] = Bp[kk * ldb + j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < RN; ++j) bv[j] = Bp[kk * ldb + j];
+        }
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
@@ -115,11 +209,20 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
       __syncthreads();
     }
     const int64_t b = b0 + tb_i * a.rb + rbi;
+    float* crow = c + b * s.sc[0] + (m0 + tm_i * RM) * s.sc[1] + (n0 + tn_i * RN) * s.sc[2];
 #pragma unroll
-    for (int i = 0; i < RM; ++i)
+    for (int i = 0; i < RM; ++i) {
+      if constexpr (RN % 4 == 0) {
+        if (a.c_vec) {
 #pragma unroll
-      for (int j = 0; j < RN; ++j)
-        c[b * s.sc[0] + (m0 + tm_i * RM + i) * s.sc[1] + (n0 + tn_i * RN + j) * s.sc[2]] = acc[i][j];
+          for (int j = 0; j < RN; j += 4)
+            *reinterpret_cast<float4*>(crow + i * s.sc[1] + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+          continue;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RN; ++j) crow[i * s.sc[1] + j * s.sc[2]] = acc[i][j];
+    }
   }
 }
 
@@ -339,12 +442,30 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
   SArgs a;
   a.s = s;
   a.tb = cfg.tb; a.tm = cfg.tm; a.tn = cfg.tn; a.rb = cfg.rb; a.bk = cfg.bk; a.kt = cfg.kt;
-  a.x_kfast = s.sx[3] == 1;
-  a.y_kfast = s.sy[3] == 1;
   a.deadline = deadline;
   a.timed_out = timed_out;
+  const int64_t bm = cfg.tm * cfg.rm, bn = cfg.tn * cfg.rn;
+  const int vw = bf16 ? 8 : 4;
+  // operand X (rows = M): contiguous along k or m?
+  a.x_kfast = s.sx[3] == 1 || s.sx[1] != 1;
+  a.y_kfast = s.sy[3] == 1 || s.sy[2] != 1;
+  auto vec_ok = [&](bool kfast, int64_t s_b, int64_t s_r, int64_t s_k, int64_t nr) {
+    if (kfast) return s_k == 1 && cfg.bk % vw == 0 && s_r % vw == 0 && s_b % vw == 0;
+    return s_r == 1 && nr % vw == 0 && s_k % vw == 0 && s_b % vw == 0;
+  };
+  a.va = vec_ok(a.x_kfast, s.sx[0], s.sx[1], s.sx[3], bm) ? vw : 1;
+  a.vb = vec_ok(a.y_kfast, s.sy[0], s.sy[2], s.sy[3], bn) ? vw : 1;
+  // k-fast staging writes columns of S[kk][r]: pad rows by one word to spread
+  // banks; r-fast staging writes rows and keeps 16-byte alignment for reads
+  a.lda = (int)(a.x_kfast ? bm + 1 : bm);
+  a.ldb = (int)(a.y_kfast ? bn + 1 : bn);
+  a.a_vec_smem = (a.lda % 4 == 0) && (cfg.rm % 4 == 0);
+  a.b_vec_smem = (a.ldb % 4 == 0) && (cfg.rn % 4 == 0);
+  a.c_vec = s.sc[2] == 1 && cfg.rn % 4 == 0 && s.sc[1] % 4 == 0 && s.sc[0] % 4 == 0;
+  const size_t smem = (((size_t)cfg.tb * cfg.bk * a.lda + 3) & ~(size_t)3) * sizeof(float) +
+                      (size_t)cfg.tb * cfg.bk * a.ldb * sizeof(float);
   dim3 grid((unsigned)cfg.gn, (unsigned)cfg.gm, (unsigned)cfg.gb);
-  return fn(x, y, c, a, grid, (int)(cfg.tb * cfg.tm * cfg.tn), (size_t)cfg.smem_bytes, st) == cudaSuccess;
+  return fn(x, y, c, a, grid, (int)(cfg.tb * cfg.tm * cfg.tn), smem, st) == cudaSuccess;
 }
 
 void launch_loopnest(const void* x, const void* y, float* c, const LoopNestCfg& cfg, bool bf16,

@@ -285,7 +285,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
   c.rb = rg[0]; c.rm = rg[1]; c.rn = rg[2];
   c.bk = bk; c.kt = kt;
   int64_t bm = c.tm * c.rm, bn = c.tn * c.rn;
-  c.smem_bytes = c.tb * c.bk * (bm + bn) * 4;
+  c.smem_bytes = c.tb * c.bk * (bm + bn + 2) * 4 + 16;  // rows padded by up to one word each
   int64_t threads = c.tb * c.tm * c.tn;
   int32_t* o = plan.cfg;
   o[0] = static_cast<int32_t>(c.gb); o[1] = static_cast<int32_t>(c.gm); o[2] = static_cast<int32_t>(c.gn);

@@ -50,7 +50,7 @@ def test_simt_mapping_matches_mlt_bands():
         assert gm * tm * rm == 512 and gn * tn * rn == 512 and bk * kt == 512
         assert (gb, tb, rb) == (1, 1, 1)
         legal = tm * tn <= 1024 and rm * rn <= 64 and rm in (1, 2, 3, 4, 6, 8, 12, 16) \
-            and rn in (1, 2, 3, 4, 6, 8, 12, 16) and bk * (tm * rm + tn * rn) * 4 <= 231 * 1024
+            and rn in (1, 2, 3, 4, 6, 8, 12, 16) and bk * (tm * rm + tn * rn + 2) * 4 + 16 <= 231 * 1024
         assert (r["status"] == "OK") == legal, r
 
 
