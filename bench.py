@@ -48,8 +48,8 @@ def load_pop(name):
 
 
 def shard(pop, rank, world, per_rank):
-    n = len(pop)
-    return [pop[(rank * per_rank + i) % n] for i in range(per_rank)]
+    from paper_2205_13603_b200.dist import shard as shard_idx
+    return [pop[i] for i in shard_idx(len(pop), rank, world, per_rank)]
 
 
 def contraction_flops(e0_json: str) -> float:
@@ -238,11 +238,11 @@ def run_b200(args):
         results.append(res)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    tot = torch.tensor([sum(devs), sum(walls)], dtype=torch.float64, device="cuda")
+    from paper_2205_13603_b200.dist import max_over_ranks
     if world > 1:
         dist.barrier()
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    dev_s, wall_s = tot[0].item() / 1e3, tot[1].item()
+    dev_ms, wall_s = max_over_ranks([sum(devs), sum(walls)], device="cuda")
+    dev_s = dev_ms / 1e3
     total_cands = len(texts) * world * args.steps
 
     # best schedule of this rank (rank 0 reports its own; all ranks see the same kinds)

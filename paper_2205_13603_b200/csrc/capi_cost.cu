@@ -1,7 +1,9 @@
 // C-ABI: batched cost model (K7) and exact simulator (K8).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -210,21 +212,96 @@ void ls_batch_destroy(ls_batch* b) {
   delete b;
 }
 
+namespace {
+
+// One persistent, growable device workspace per device for the one-shot
+// entry points (the search calls them once per new program, so per-call
+// allocation would dominate).
+struct Workspace {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  int64_t *blobs = nullptr, *off = nullptr, *num = nullptr, *den = nullptr;
+  double *feats = nullptr, *pred = nullptr;
+  int32_t* status = nullptr;
+  size_t cap_words = 0, cap_n = 0;
+};
+Workspace g_ws[64];
+
+ls_status grow(Workspace& w, size_t words, size_t n) {
+  if (!w.stream) LSB_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+  if (words > w.cap_words) {
+    cudaFree(w.blobs);
+    w.blobs = nullptr;
+    size_t c = std::max(words, 2 * w.cap_words);
+    LSB_CUDA(cudaMalloc(&w.blobs, c * 8));
+    w.cap_words = c;
+  }
+  if (n > w.cap_n) {
+    cudaFree(w.off); cudaFree(w.num); cudaFree(w.den); cudaFree(w.feats); cudaFree(w.pred); cudaFree(w.status);
+    w.off = w.num = w.den = nullptr; w.feats = w.pred = nullptr; w.status = nullptr;
+    size_t c = std::max(n, 2 * w.cap_n);
+    LSB_CUDA(cudaMalloc(&w.off, (c + 1) * 8));
+    LSB_CUDA(cudaMalloc(&w.num, c * 8));
+    LSB_CUDA(cudaMalloc(&w.den, c * 8));
+    LSB_CUDA(cudaMalloc(&w.feats, c * 9 * 8));
+    LSB_CUDA(cudaMalloc(&w.pred, c * 8));
+    LSB_CUDA(cudaMalloc(&w.status, c * 4));
+    w.cap_n = c;
+  }
+  return LS_OK;
+}
+
+}  // namespace
+
 ls_status ls_analyze_batch(int device, const char* const* programs, const size_t* lens, int n,
                            const ls_machine_spec* spec, const ls_linear_model* model, int64_t* num, int64_t* den,
                            double* feats, double* pred, int32_t* status) {
-  if (!spec) {
-    set_error("ls_analyze_batch: null machine spec");
+  if (!spec || n < 0 || (n > 0 && (!programs || !lens))) {
+    set_error("ls_analyze_batch: bad arguments");
     return LS_ERR_ARG;
   }
-  ls_batch* b = nullptr;
-  ls_status st = ls_batch_create(device, programs, lens, n, &b);
+  ls_status st = use_device(device);
   if (st != LS_OK) return st;
+  if (device >= 64) {
+    set_error("ls_analyze_batch: device index above 63");
+    return LS_ERR_ARG;
+  }
+  if (n == 0) return LS_OK;
+  std::vector<std::vector<int64_t>> blobs(static_cast<size_t>(n));
+  parallel_for(n, [&](int i) {
+    std::string err;
+    auto p = parse_program(std::string_view(programs[i], lens[i]), &err);
+    std::vector<int64_t>& b = blobs[static_cast<size_t>(i)];
+    if (!p) {
+      b.assign(HDR_WORDS, 0);
+      b[H_STATUS] = LS_PROG_PARSE;
+    } else if (!encode_cost_blob(*p, &b, &err)) {
+      b.assign(HDR_WORDS, 0);
+      b[H_STATUS] = LS_PROG_ANALYSIS;
+    }
+  });
+  std::vector<int64_t> offsets(static_cast<size_t>(n) + 1, 0);
+  for (int i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + static_cast<int64_t>(blobs[i].size());
+  std::vector<int64_t> flat(static_cast<size_t>(offsets[n]));
+  for (int i = 0; i < n; ++i) std::copy(blobs[i].begin(), blobs[i].end(), flat.begin() + offsets[i]);
+
+  Workspace& w = g_ws[device];
+  std::lock_guard<std::mutex> lock(w.mu);
+  if ((st = grow(w, flat.size(), static_cast<size_t>(n))) != LS_OK) return st;
+  const size_t nn = static_cast<size_t>(n);
+  LSB_CUDA(cudaMemcpyAsync(w.blobs, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, w.stream));
+  LSB_CUDA(cudaMemcpyAsync(w.off, offsets.data(), (nn + 1) * 8, cudaMemcpyHostToDevice, w.stream));
   int flags = (num || den ? 1 : 0) | (feats ? 2 : 0) | (pred && model ? 4 : 0);
-  st = ls_batch_analyze(b, spec, model, flags);
-  if (st == LS_OK) st = ls_batch_results(b, num, den, feats, pred, status);
-  ls_batch_destroy(b);
-  return st;
+  launch_analyze(w.blobs, w.off, n, to_dspec(spec), to_dmodel(model), flags, w.num, w.den, w.feats, w.pred,
+                 w.status, w.stream);
+  LSB_CUDA(cudaGetLastError());
+  if (num) LSB_CUDA(cudaMemcpyAsync(num, w.num, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (den) LSB_CUDA(cudaMemcpyAsync(den, w.den, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (feats) LSB_CUDA(cudaMemcpyAsync(feats, w.feats, nn * 72, cudaMemcpyDeviceToHost, w.stream));
+  if (pred && model) LSB_CUDA(cudaMemcpyAsync(pred, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (status) LSB_CUDA(cudaMemcpyAsync(status, w.status, nn * 4, cudaMemcpyDeviceToHost, w.stream));
+  LSB_CUDA(cudaStreamSynchronize(w.stream));
+  return LS_OK;
 }
 
 ls_status ls_sim_latency_batch(int device, const char* const* programs, const size_t* lens, int n,
@@ -253,21 +330,19 @@ ls_status ls_score_batch(int device, const double* feats, int n, const ls_linear
   ls_status st = use_device(device);
   if (st != LS_OK) return st;
   if (n == 0) return LS_OK;
-  double *d_f = nullptr, *d_o = nullptr;
-  LSB_CUDA(cudaMalloc(&d_f, static_cast<size_t>(n) * 9 * 8));
-  cudaError_t e = cudaMalloc(&d_o, static_cast<size_t>(n) * 8);
-  if (e == cudaSuccess) e = cudaMemcpy(d_f, feats, static_cast<size_t>(n) * 9 * 8, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) {
-    launch_score(d_f, n, to_dmodel(model), d_o, nullptr);
-    e = cudaGetLastError();
+  if (device >= 64) {
+    set_error("ls_score_batch: device index above 63");
+    return LS_ERR_ARG;
   }
-  if (e == cudaSuccess) e = cudaMemcpy(out, d_o, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost);
-  cudaFree(d_f);
-  cudaFree(d_o);
-  if (e != cudaSuccess) {
-    set_error(std::string("ls_score_batch: ") + cudaGetErrorString(e));
-    return LS_ERR_CUDA;
-  }
+  Workspace& w = g_ws[device];
+  std::lock_guard<std::mutex> lock(w.mu);
+  if ((st = grow(w, 1, static_cast<size_t>(n))) != LS_OK) return st;
+  const size_t nn = static_cast<size_t>(n);
+  LSB_CUDA(cudaMemcpyAsync(w.feats, feats, nn * 72, cudaMemcpyHostToDevice, w.stream));
+  launch_score(w.feats, n, to_dmodel(model), w.pred, w.stream);
+  LSB_CUDA(cudaGetLastError());
+  LSB_CUDA(cudaMemcpyAsync(out, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  LSB_CUDA(cudaStreamSynchronize(w.stream));
   return LS_OK;
 }
 

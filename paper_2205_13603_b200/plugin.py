@@ -1,0 +1,137 @@
+"""Drop-in installation of the B200 path into the reference's search.
+
+The reference's search driver (`tune` / `evolve` / `mutate` / `mh_accept`,
+`src/search.py:162-376`) stays unchanged; for the duration of ``installed()``
+(or one ``tune(...)`` call) its four seams are rebound:
+
+  ======================================  ===========================================
+  reference seam                          B200 implementation
+  ======================================  ===========================================
+  ``search._measure_batch`` (:249-256,    ``Runner.measure``: hardware (``B200Runner``,
+  called at :345)                         ``ShardedRunner``) or parity (``SimRunner``)
+  ``search.simulate_latency`` (baseline,  ``Runner.baseline``
+  :326)
+  ``search.featurize`` (:141)             K7 on the GPU, memoized by program text
+  ``_Validator._predict`` (:109-111; the  K7b: every known feature row rescored in
+  reference's own plug-in seam,           one launch per model, then lookups
+  tests/test_search.py:125-127)
+  ======================================  ===========================================
+
+Nothing in the reference is edited or copied; the originals are restored on
+exit even when the search raises.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from fractions import Fraction
+
+import numpy as np
+
+from .inputs import program_text
+from .refapi import loopsched
+
+
+class SimRunner:
+    """Parity-mode Runner: the reference's simulated latency, computed exactly
+    (int128 rationals) by the K8 kernel -- bit-identical to
+    ``simulate_latency`` (`src/machine.py:228-254`)."""
+
+    def __init__(self, device: int = 0, scorer=None):
+        from .scorer import GpuScorer
+        self.scorer = scorer or GpuScorer(device)
+
+    def measure(self, candidates, machine_spec=None, jobs: int = 1) -> list:
+        if not candidates:
+            return []
+        return self.scorer.sim_latency_batch(candidates, machine_spec)
+
+    def baseline(self, e0, machine_spec=None) -> Fraction:
+        return self.scorer.sim_latency_batch([e0], machine_spec)[0]
+
+
+class ScoreCache:
+    """K7 features memoized by program text; predictions memoized per model
+    (a new model triggers one batched K7b launch over every known row)."""
+
+    def __init__(self, scorer):
+        self.scorer = scorer
+        self.features: dict[str, np.ndarray] = {}
+        self._model = None
+        self._scores: dict[bytes, float] = {}
+        self.launches = 0
+
+    def featurize(self, program, machine_spec=None) -> np.ndarray:
+        text = program_text(program)
+        f = self.features.get(text)
+        if f is None:
+            f = self.scorer.featurize_batch([text], machine_spec)[0]
+            self.launches += 1
+            self.features[text] = f
+        return f.copy()
+
+    def predict(self, features, model) -> float:
+        if model is not self._model:
+            self._model = model
+            self._scores = {}
+            rows = {f.tobytes(): f for f in self.features.values()}
+            if rows:
+                keys = list(rows)
+                vals = self.scorer.score_batch(np.stack([rows[k] for k in keys]), model)
+                self.launches += 1
+                self._scores = dict(zip(keys, map(float, vals)))
+        f = np.asarray(features, dtype=np.float64)
+        key = f.tobytes()
+        s = self._scores.get(key)
+        if s is None:
+            s = float(self.scorer.score_batch(f.reshape(1, 9), model)[0])
+            self.launches += 1
+            self._scores[key] = s
+        return s
+
+
+@contextlib.contextmanager
+def installed(runner=None, scorer=None):
+    """Rebind the reference's seams to ``runner`` (Runner protocol) and
+    ``scorer`` (Scorer protocol) inside the block."""
+    ls = loopsched()
+    S = ls.search
+    saved = (S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict)
+    cache = ScoreCache(scorer) if scorer is not None else None
+    try:
+        if runner is not None:
+            S._measure_batch = lambda cands, spec, jobs: runner.measure(cands, spec, jobs)
+            S.simulate_latency = lambda p, spec=None: runner.baseline(p, spec)
+        if cache is not None:
+            S.featurize = lambda p, spec=None: cache.featurize(p, spec)
+            S._Validator._predict = lambda self, program, features, model: cache.predict(features, model)
+        yield cache
+    finally:
+        S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict = saved
+
+
+def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
+         mode: str = "hardware", runner=None, scorer=None, device: int = 0, dtype: str = "bf16",
+         **runner_opts):
+    """The reference's ``tune`` with the B200 seams installed.
+
+    mode "hardware": candidates are instantiated and timed on the GPU
+    (latencies in ns); mode "parity": latencies are the reference's simulated
+    cycles computed exactly on the GPU, so the search makes the same decisions
+    as the CPU reference for the same seed."""
+    ls = loopsched()
+    from .scorer import GpuScorer
+    config = config or ls.SearchConfig()
+    machine_spec = machine_spec or ls.MachineSpec()
+    scorer = scorer or GpuScorer(device)
+    if runner is None:
+        if mode == "parity":
+            runner = SimRunner(device, scorer)
+        elif mode == "hardware":
+            from .runner import B200Runner
+            runner = B200Runner(device=device, dtype=dtype, **runner_opts)
+            runner.set_workload(e0)
+        else:
+            raise ValueError(f"unknown mode {mode!r}")
+    with installed(runner, scorer):
+        return ls.search.tune(e0, generator, config, machine_spec, warm_records)

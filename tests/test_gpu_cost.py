@@ -78,3 +78,43 @@ def test_parse_failure_is_reported(scorer):
     from paper_2205_13603_b200.scorer import AnalysisError
     with pytest.raises(AnalysisError):
         scorer.analyze(["{bad json"])
+
+
+@pytest.mark.parametrize("name", ["gmm512", "gmm512_tu", "bert_ffn"])
+def test_parity_mode_reproduces_reference_tune_log(scorer, name):
+    """Chosen-trace parity: every program the reference tune measured gets the
+    identical latency from K8 (and features from K7), so ranking, refits and
+    the chosen best trace are the reference's own."""
+    import json
+    import os
+    from conftest import GOLDEN
+    doc = json.load(open(os.path.join(GOLDEN, f"tune_{name}.json")))
+    progs = doc["log_programs"]
+    lats, feats, _ = scorer.analyze(progs)
+    for lat, rec in zip(lats, doc["log"]):
+        assert str(lat) == rec["exact"]
+    np.testing.assert_allclose(feats, np.array([r["features"] for r in doc["log"]]), rtol=1e-14, atol=0)
+    best = min(range(len(lats)), key=lambda i: lats[i])
+    assert doc["log"][best]["trace"] == doc["best"]["trace"]["instructions"]
+    base = scorer.sim_latency_batch([doc["e0"]])[0]
+    assert str(base) == doc["baseline"]["exact"]
+
+
+def test_score_cache_plugin_path(scorer):
+    from paper_2205_13603_b200.plugin import ScoreCache, SimRunner
+    rows = load_programs()[:20]
+    model = load_model()
+    cache = ScoreCache(scorer)
+    for r in rows:
+        f = cache.featurize(r["program"])
+        np.testing.assert_allclose(f, r["features"], rtol=1e-14)
+    for r in rows:
+        assert cache.predict(np.array(r["features"]), model) == pytest.approx(r["predicted"], rel=1e-12)
+    sim = SimRunner(0, scorer)
+
+    class C:
+        def __init__(self, p):
+            self.program = p
+
+    lats = sim.measure([C(r["program"]) for r in rows])
+    assert [str(l) for l in lats] == [str(Fraction(*r["latency"])) for r in rows]
