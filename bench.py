@@ -304,7 +304,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
     ap.add_argument("--cpu-budget", type=float, default=8.0)
-    ap.add_argument("--timeout-factor", type=float, default=20.0,
+    ap.add_argument("--timeout-factor", type=float, default=10.0,
                     help="checked launches get clamp(factor x best-so-far, 0.05 ms, 2 x e0) before abort")
     args = ap.parse_args()
     if args.impl == "reference":
