@@ -255,6 +255,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       c[4] = static_cast<int32_t>(t.splits); c[5] = static_cast<int32_t>(t.kt);
       c[6] = static_cast<int32_t>(t.stages); c[7] = static_cast<int32_t>(t.smem_bytes / 1024);
       if (t.bn > 256) return illegal(plan, "UMMA N above 256");
+      if (t.smem_bytes > lim.max_smem) return illegal(plan, "shared-memory ring + reduction buffer above 227 KB");
       if (t.batch * t.splits > 65535 || t.grid_m > 65535) return illegal(plan, "grid too large");
       return plan;
     }
