@@ -38,6 +38,7 @@ WORKLOADS = {
     "bert_ffn": ("pop_bert_ffn.jsonl.gz", "bf16", "BERT-base dense GEMM 128x768x3072 bf16 with tcgen05 tensorize"),
     "bmm_qk": ("pop_bmm_qk.jsonl.gz", "bf16", "BERT-base attention batch_matmul 12x128x128x64 bf16"),
     "gmm512": ("pop_gmm512.jsonl.gz", "f32", "GEMM 512x512x512 fp32"),
+    "conv2d": ("pop_conv2d.jsonl.gz", "bf16", "ResNet-50 conv2d 56x56x64->64 3x3 NHWC bf16 implicit GEMM"),
 }
 
 
@@ -53,13 +54,14 @@ def shard(pop, rank, world, per_rank):
 
 
 def contraction_flops(e0_json: str) -> float:
-    """2 x the iteration count of the (single-block) unscheduled contraction."""
+    """2 x the iteration count of the unscheduled contraction block (the
+    reduction block; elementwise stages such as a pad are not counted)."""
     def walk(stmts):
         tot = 0
         for st in stmts:
             if "loop" in st:
                 tot += st["loop"]["extent"] * walk(st["loop"]["body"])
-            else:
+            elif "compute" in st and "init" in st["compute"]:
                 tot += 1
         return tot
     return 2.0 * walk(json.loads(e0_json)["root"])

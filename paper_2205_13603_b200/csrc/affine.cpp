@@ -1,0 +1,409 @@
+// Planner for general workloads.  See affine.hpp.
+#include "affine.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <random>
+
+#include "plan.hpp"
+
+namespace lsb {
+
+namespace {
+
+const int64_t kATiles[] = {1, 2, 3, 4, 6, 7, 8, 12, 14, 16};
+constexpr int kNATiles = 10;
+
+// witness kinds: the access whose index at `dim` is exactly the axis variable
+enum WKind { W_STORE = 0, W_Y = 1, W_X = 2 };
+
+bool fail(std::string* err, const std::string& m) {
+  if (err) *err = m;
+  return false;
+}
+
+int exact_dim(const std::vector<Expr*>& idx, int var) {
+  for (size_t d = 0; d < idx.size(); ++d)
+    if (idx[d]->op == Op::Var && idx[d]->var == var) return static_cast<int>(d);
+  return -1;
+}
+
+bool has_var(const std::vector<Expr*>& idx, int var) {
+  std::vector<int> vs;
+  for (const Expr* e : idx) expr_vars(e, &vs);
+  return std::find(vs.begin(), vs.end(), var) != vs.end();
+}
+
+int64_t host_eval(const Expr* e, const std::vector<int64_t>& vals, bool* ok) {
+  switch (e->op) {
+    case Op::Int: return e->value;
+    case Op::Var: return vals[static_cast<size_t>(e->var)];
+    case Op::Load: *ok = false; return 0;
+    case Op::Select: {
+      int64_t c = host_eval(e->kids[0], vals, ok);
+      return c != 0 ? host_eval(e->kids[1], vals, ok) : host_eval(e->kids[2], vals, ok);
+    }
+    default: break;
+  }
+  int64_t a = host_eval(e->kids[0], vals, ok), b = host_eval(e->kids[1], vals, ok);
+  switch (e->op) {
+    case Op::Add: return a + b;
+    case Op::Sub: return a - b;
+    case Op::Mul: return a * b;
+    case Op::Max: return std::max(a, b);
+    case Op::Min: return std::min(a, b);
+    case Op::FloorDiv: { int64_t q = a / b; if ((a % b) && ((a < 0) != (b < 0))) --q; return q; }
+    case Op::Mod: { int64_t r = a % b; if (r && ((r < 0) != (b < 0))) r += b; return r; }
+    default: *ok = false; return 0;
+  }
+}
+
+// The X-side factor of a contraction value: a Load, or Select(cond, Load, 0).
+bool x_side(const Expr* f, const Expr** load, const Expr** cond) {
+  if (f->op == Op::Load) { *load = f; *cond = nullptr; return true; }
+  if (f->op == Op::Select && f->kids[1]->op == Op::Load && f->kids[2]->op == Op::Int && f->kids[2]->value == 0) {
+    *load = f->kids[1];
+    *cond = f->kids[0];
+    return true;
+  }
+  return false;
+}
+
+GeneralPlan unsupported(const char* why) {
+  GeneralPlan g;
+  g.status = P_UNSUPPORTED;
+  g.why = why;
+  return g;
+}
+
+}  // namespace
+
+int simta_tile_index(int64_t v) {
+  for (int i = 0; i < kNATiles; ++i)
+    if (kATiles[i] == v) return i;
+  return -1;
+}
+
+bool simta_tile_supported(int64_t rm, int64_t rn) {
+  return simta_tile_index(rm) >= 0 && simta_tile_index(rn) >= 0 && rm * rn <= 64;
+}
+
+bool analyze_general(const Program& e0, GeneralWorkload* w, std::string* err) {
+  std::vector<Block> blocks = blocks_preorder(e0);
+  const Block* con = nullptr;
+  for (const Block& b : blocks) {
+    if (b.stmt->type != SType::Compute) return fail(err, "intrinsic blocks are not supported");
+    if (b.stmt->init) {
+      if (con) return fail(err, "more than one reduction block");
+      con = &b;
+    }
+  }
+  if (!con) return fail(err, "no contraction block");
+  const Stmt* s = con->stmt;
+  if (s->init->op != Op::Int || s->init->value != 0 || s->epilogue)
+    return fail(err, "contraction must start from 0 without an epilogue in e0");
+  const Expr* v = s->value;
+  if (v->op != Op::Mul || v->kids[0]->op != Op::Load || v->kids[1]->op != Op::Load)
+    return fail(err, "contraction value must be a product of two loads");
+  const Expr* a = v->kids[0];
+  const Expr* b = v->kids[1];
+  w->block = s->name;
+  w->x_buf = e0.buffers[static_cast<size_t>(a->buffer)].name;
+  w->y_buf = e0.buffers[static_cast<size_t>(b->buffer)].name;
+  w->c_buf = e0.buffers[static_cast<size_t>(s->buffer)].name;
+  for (const Stmt* l : con->loops) {
+    bool sp = has_var(s->indices, l->var);
+    bool in_a = has_var(a->kids, l->var), in_b = has_var(b->kids, l->var);
+    int group;
+    if (sp) group = in_a && in_b ? AG_B : in_a ? AG_M : in_b ? AG_N : -1;
+    else group = (in_a || in_b) ? AG_K : -1;
+    if (group < 0) return fail(err, "loop variable outside the contraction pattern");
+    std::string wb;
+    int wd = -1;
+    if (sp && (wd = exact_dim(s->indices, l->var)) >= 0) wb = "store";
+    else if ((wd = exact_dim(b->kids, l->var)) >= 0) wb = "y";
+    else if ((wd = exact_dim(a->kids, l->var)) >= 0) wb = "x";
+    else return fail(err, "no access indexed by exactly one axis variable");
+    w->axis_var.push_back(e0.vars[static_cast<size_t>(l->var)]);
+    w->axis_group.push_back(group);
+    w->axis_extent.push_back(l->extent);
+    w->wit_buf.push_back(wb);
+    w->wit_dim.push_back(wd);
+  }
+  for (const Buffer& B : e0.buffers) {
+    w->buffers.push_back(B.name);
+    w->shapes.push_back(B.shape);
+    w->roles.push_back(B.role);
+    if (B.name == w->c_buf) {
+      int64_t n = 1;
+      for (int64_t x : B.shape) n *= x;
+      w->c_elems = n;
+    }
+  }
+  return true;
+}
+
+GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const DeviceLimits& lim) {
+  GeneralPlan plan;
+  std::string err;
+  if (!encode_generic(p, &plan.gen, &err)) return unsupported("program is not executable by the generic executor");
+  for (const Buffer& B : p.buffers) plan.buf_names.push_back(B.name);
+  for (const std::string& n : plan.buf_names)
+    if (std::find(w.buffers.begin(), w.buffers.end(), n) == w.buffers.end())
+      return unsupported("candidate introduces a buffer the workload does not have");
+  std::vector<Block> blocks = blocks_preorder(p);
+  bool seen_con = false;
+  for (size_t bi = 0; bi < blocks.size(); ++bi) {
+    const Block& blk = blocks[bi];
+    const Stmt* s = blk.stmt;
+    GStep step;
+    step.block = static_cast<int>(bi);
+    if (!s->init) {
+      step.family = F_GENERIC;
+      plan.steps.push_back(step);
+      continue;
+    }
+    if (s->name != w.block || seen_con) return unsupported("unexpected reduction block");
+    seen_con = true;
+    const Expr* v = s->value;
+    if (v->op != Op::Mul) return unsupported("contraction value changed shape");
+    const Expr* yl = nullptr;
+    const Expr* xf = nullptr;
+    for (int i = 0; i < 2; ++i)
+      if (v->kids[i]->op == Op::Load && p.buffers[static_cast<size_t>(v->kids[i]->buffer)].name == w.y_buf) {
+        yl = v->kids[i];
+        xf = v->kids[1 - i];
+      }
+    const Expr* xl = nullptr;
+    const Expr* cond = nullptr;
+    if (!yl || !x_side(xf, &xl, &cond)) return unsupported("contraction operands changed shape");
+
+    // PVU-scheduled contraction (possibly fused loops): generic nest kernel
+    bool block_serial = true;
+    for (const Stmt* l : blk.loops) block_serial &= l->kind == Kind::Serial;
+    if (!block_serial) {
+      if (blk.loops.empty() || blk.loops[0]->kind != Kind::Parallel)
+        return unsupported("parallel loop is not outermost");
+      step.family = F_NESTGEN;
+      plan.family = F_NESTGEN;
+      plan.cfg[0] = static_cast<int32_t>(blk.loops[0]->extent);
+      plan.steps.push_back(step);
+      if (s->epilogue) {
+        GStep e = step;
+        e.family = F_GENERIC;
+        e.epilogue_pass = true;
+        plan.steps.push_back(e);
+      }
+      continue;
+    }
+
+    // per-loop axis and stride from the witness expressions
+    const size_t nv = p.vars.size();
+    const size_t na = w.axis_var.size();
+    std::vector<std::vector<int64_t>> coef(na);
+    for (size_t a = 0; a < na; ++a) {
+      const std::vector<Expr*>* idx = w.wit_buf[a] == "store" ? &s->indices
+                                    : w.wit_buf[a] == "y" ? &yl->kids : &xl->kids;
+      if (static_cast<size_t>(w.wit_dim[a]) >= idx->size()) return unsupported("witness dim missing");
+      int64_t c0 = 0;
+      if (!affine_coeffs((*idx)[static_cast<size_t>(w.wit_dim[a])], nv, &coef[a], &c0) || c0 != 0)
+        return unsupported("non-affine index (fused loop) in the contraction");
+    }
+    struct LP { int axis; int64_t ext, stride; Kind kind; int var; };
+    std::vector<LP> lps;
+    for (const Stmt* l : blk.loops) {
+      int axis = -1;
+      int64_t stride = 0;
+      for (size_t a = 0; a < na; ++a) {
+        if (coef[a][static_cast<size_t>(l->var)] == 0) continue;
+        if (axis >= 0) { axis = -2; break; }
+        axis = static_cast<int>(a);
+        stride = coef[a][static_cast<size_t>(l->var)];
+      }
+      if (axis == -2) return unsupported("loop variable feeds two axes");
+      if (axis < 0) {
+        if (l->extent == 1) continue;
+        return unsupported("loop variable unused by the contraction");
+      }
+      lps.push_back(LP{axis, l->extent, stride, l->kind, l->var});
+    }
+    bool any_parallel = false, all_serial = true;
+    for (const LP& q : lps) {
+      all_serial &= q.kind == Kind::Serial;
+      any_parallel |= q.kind == Kind::Parallel;
+    }
+    if (!all_serial) {
+      // PVU: the outermost loop of the block must be the parallel one
+      if (blk.loops.empty() || blk.loops[0]->kind != Kind::Parallel || !any_parallel)
+        return unsupported("parallel loop is not outermost");
+      step.family = F_NESTGEN;
+      plan.family = F_NESTGEN;
+      plan.cfg[0] = static_cast<int32_t>(blk.loops[0]->extent);
+      plan.steps.push_back(step);
+      if (s->epilogue) {
+        GStep e = step;
+        e.family = F_GENERIC;
+        e.epilogue_pass = true;
+        plan.steps.push_back(e);
+      }
+      continue;
+    }
+    for (size_t a = 0; a < na; ++a) {
+      int64_t inner = 1;
+      for (size_t i = lps.size(); i-- > 0;) {
+        if (lps[i].axis != static_cast<int>(a)) continue;
+        if (lps[i].stride != inner) return unsupported("axis parts not in split order");
+        inner *= lps[i].ext;
+      }
+      if (inner != w.axis_extent[a]) return unsupported("axis parts do not cover the axis");
+    }
+    std::vector<int> nparts(na, 0);
+    for (const LP& q : lps) nparts[static_cast<size_t>(q.axis)]++;
+    bool naive = true;
+    for (int c : nparts) naive &= c <= 1;
+    if (naive) {
+      step.family = F_GENERIC;
+      plan.family = F_NAIVE;
+      plan.steps.push_back(step);
+      if (s->epilogue) {
+        GStep e = step;
+        e.epilogue_pass = true;
+        plan.steps.push_back(e);
+      }
+      continue;
+    }
+    for (int g : w.axis_group)
+      if (g == AG_B) return unsupported("batch axes are instantiated by the SIMT family of single-axis workloads");
+
+    // ---- SIMT-A: address coefficients per loop ----
+    AffineCfg& A = step.aff;
+    std::memset(&A, 0, sizeof A);
+    auto strides_of = [&](int buf) {
+      const Buffer& B = p.buffers[static_cast<size_t>(buf)];
+      std::vector<int64_t> st(B.shape.size(), 1);
+      for (size_t d = B.shape.size(); d-- > 1;) st[d - 1] = st[d] * B.shape[d];
+      return st;
+    };
+    auto lin = [&](const std::vector<Expr*>& idx, int buf, std::vector<int64_t>* per_var, int64_t* c0) {
+      std::vector<int64_t> st = strides_of(buf);
+      per_var->assign(nv, 0);
+      *c0 = 0;
+      for (size_t d = 0; d < idx.size(); ++d) {
+        std::vector<int64_t> c;
+        int64_t k0;
+        if (!affine_coeffs(idx[d], nv, &c, &k0)) return false;
+        for (size_t x = 0; x < nv; ++x) (*per_var)[x] += st[d] * c[x];
+        *c0 += st[d] * k0;
+      }
+      return true;
+    };
+    std::vector<int64_t> cx, cy, cc;
+    if (!lin(xl->kids, xl->buffer, &cx, &A.x0) || !lin(yl->kids, yl->buffer, &cy, &A.y0) ||
+        !lin(s->indices, s->buffer, &cc, &A.c0))
+      return unsupported("non-affine operand index");
+    // guarded X dims (inlined pad): dims whose index range leaves the buffer
+    std::vector<int> gdims;
+    std::vector<std::vector<int64_t>> gcoef;
+    std::vector<int64_t> gconst;
+    const Buffer& XB = p.buffers[static_cast<size_t>(xl->buffer)];
+    for (size_t d = 0; d < xl->kids.size(); ++d) {
+      std::vector<int64_t> c;
+      int64_t k0;
+      affine_coeffs(xl->kids[d], nv, &c, &k0);
+      int64_t lo = k0, hi = k0;
+      for (const LP& q : lps) {
+        int64_t t = c[static_cast<size_t>(q.var)] * (q.ext - 1);
+        if (t < 0) lo += t; else hi += t;
+      }
+      if (lo < 0 || hi >= XB.shape[d]) {
+        if (!cond) return unsupported("operand index leaves its buffer");
+        gdims.push_back(static_cast<int>(d));
+        gcoef.push_back(c);
+        gconst.push_back(k0);
+      }
+    }
+    if (gdims.size() > 2) return unsupported("more than two guarded dims");
+    if (cond) {
+      // the Select guard must be exactly the in-bounds predicate of the load:
+      // checked on the corners and a deterministic sample of the iteration space
+      std::mt19937_64 rng(12345);
+      std::vector<int64_t> vals(nv, 0);
+      for (int t = 0; t < 256; ++t) {
+        for (const LP& q : lps) {
+          int64_t x = t == 0 ? 0 : t == 1 ? q.ext - 1 : static_cast<int64_t>(rng() % static_cast<uint64_t>(q.ext));
+          vals[static_cast<size_t>(q.var)] = x;
+        }
+        bool ok = true;
+        int64_t cv = host_eval(cond, vals, &ok);
+        bool inb = true;
+        for (size_t d = 0; d < xl->kids.size(); ++d) {
+          int64_t x = host_eval(xl->kids[d], vals, &ok);
+          inb &= x >= 0 && x < XB.shape[d];
+        }
+        if (!ok || ((cv != 0) != inb)) return unsupported("Select guard is not the load's in-bounds predicate");
+      }
+    }
+    A.ng = static_cast<int>(gdims.size());
+    for (int g = 0; g < A.ng; ++g) {
+      A.g0[g] = gconst[static_cast<size_t>(g)];
+      A.gext[g] = XB.shape[static_cast<size_t>(gdims[static_cast<size_t>(g)])];
+    }
+    // levels: spatial band 0 grid, 1 threads, >= 2 registers; K last part BK
+    std::vector<int> band(na, 0), seenk(na, 0);
+    if (lps.size() > static_cast<size_t>(kAMaxParts)) return unsupported("too many loops");
+    A.nparts = static_cast<int>(lps.size());
+    A.gm = A.gn = A.tm = A.tn = A.rm = A.rn = A.bk = A.kt = 1;
+    for (size_t i = 0; i < lps.size(); ++i) {
+      const LP& q = lps[i];
+      APart& P = A.parts[i];
+      P.extent = q.ext;
+      P.group = w.axis_group[static_cast<size_t>(q.axis)];
+      P.cx = cx[static_cast<size_t>(q.var)];
+      P.cy = cy[static_cast<size_t>(q.var)];
+      P.cc = cc[static_cast<size_t>(q.var)];
+      for (int g = 0; g < A.ng; ++g) P.cg[g] = gcoef[static_cast<size_t>(g)][static_cast<size_t>(q.var)];
+      if (P.group == AG_K) {
+        int idx = ++seenk[static_cast<size_t>(q.axis)];
+        P.level = idx == nparts[static_cast<size_t>(q.axis)] ? AL_BK : AL_KTILE;
+        if (P.level == AL_BK) A.bk *= q.ext; else A.kt *= q.ext;
+      } else {
+        int b = band[static_cast<size_t>(q.axis)]++;
+        P.level = b == 0 ? AL_GRID : b == 1 ? AL_THREAD : AL_REG;
+        int64_t& grid = P.group == AG_M ? A.gm : A.gn;
+        int64_t& thr = P.group == AG_M ? A.tm : A.tn;
+        int64_t& reg = P.group == AG_M ? A.rm : A.rn;
+        (P.level == AL_GRID ? grid : P.level == AL_THREAD ? thr : reg) *= q.ext;
+      }
+    }
+    const int64_t bm = A.tm * A.rm, bn = A.tn * A.rn;
+    A.smem_bytes = A.bk * (bm + 1 + bn + 1) * 4 + 16 + (2 * bm + 2 * A.bk + 2 * bn + 2 * (bm + A.bk)) * 4 + 64;
+    step.family = F_SIMTA;
+    step.x_buf = xl->buffer;
+    step.y_buf = yl->buffer;
+    step.c_buf = s->buffer;
+    plan.family = F_SIMTA;
+    int32_t* o = plan.cfg;
+    o[0] = 1; o[1] = static_cast<int32_t>(A.gm); o[2] = static_cast<int32_t>(A.gn);
+    o[3] = 1; o[4] = static_cast<int32_t>(A.tm); o[5] = static_cast<int32_t>(A.tn);
+    o[6] = 1; o[7] = static_cast<int32_t>(A.rm); o[8] = static_cast<int32_t>(A.rn);
+    o[9] = static_cast<int32_t>(A.bk); o[10] = static_cast<int32_t>(A.kt);
+    o[11] = static_cast<int32_t>(A.smem_bytes / 1024); o[12] = static_cast<int32_t>(A.tm * A.tn);
+    plan.steps.push_back(step);
+    if (A.tm * A.tn > lim.max_threads) { plan.status = P_ILLEGAL; plan.why = "threads per CTA above 1024"; return plan; }
+    if (!simta_tile_supported(A.rm, A.rn)) { plan.status = P_ILLEGAL; plan.why = "register tile outside the lattice"; return plan; }
+    if (A.smem_bytes > lim.max_smem) { plan.status = P_ILLEGAL; plan.why = "shared-memory tile above 227 KB"; return plan; }
+    if (A.gm > 65535) { plan.status = P_ILLEGAL; plan.why = "grid too large"; return plan; }
+    if (s->epilogue) {
+      GStep e;
+      e.family = F_GENERIC;
+      e.block = static_cast<int>(bi);
+      e.epilogue_pass = true;
+      plan.steps.push_back(e);
+    }
+  }
+  if (!seen_con) return unsupported("candidate lost its contraction block");
+  plan.status = P_OK;
+  return plan;
+}
+
+}  // namespace lsb

@@ -30,8 +30,11 @@
 #include "../../include/loopsched_b200.h"
 #include "common.hpp"
 #include "ir.hpp"
+#include "affine.hpp"
+#include "generic.cuh"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "simta.cuh"
 
 using namespace lsb;
 
@@ -109,6 +112,11 @@ struct ls_runner {
   ~ls_runner() { release(); }
 
   void release_workload() {
+    for (size_t i = 0; i < gbuf.size(); ++i)
+      if (gbuf[i] != c) cudaFree(gbuf[i]);
+    gbuf.clear();
+    gbuf_dtype.clear();
+    general = false;
     cudaFree(x); cudaFree(y); cudaFree(yk); cudaFree(c); cudaFree(ref);
     x = y = yk = nullptr; c = nullptr; ref = nullptr;
     tmap_b.clear();
@@ -118,7 +126,8 @@ struct ls_runner {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
     release_workload();
-    cudaFree(deadline); cudaFree(flags); cudaFree(parity);
+    cudaFree(deadline); cudaFree(flags); cudaFree(parity); cudaFree(gcode);
+    gcode = nullptr;
     deadline = nullptr; flags = nullptr; parity = nullptr;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
@@ -154,10 +163,64 @@ struct ls_runner {
 
   // one launch of a planned candidate (plus its zeroing memset)
   unsigned long long* trace = nullptr;  // set only by ls_runner_trace_tc
+  // general workloads (multi-block / affine contraction)
+  bool general = false;
+  GeneralWorkload gw;
+  std::vector<void*> gbuf;      // device buffer per e0 buffer (gw.buffers order)
+  std::vector<int> gbuf_dtype;  // 0 bf16, 1 f32
+  int64_t* gcode = nullptr;     // concatenated bytecode of the current batch
+  size_t gcode_cap = 0;
+
+  bool general_buffers(const Plan& p, GenBuffers* B) {
+    const GenProgram& g = p.gp->gen;
+    std::memset(B, 0, sizeof *B);
+    for (int b = 0; b < g.nbuf; ++b) {
+      const std::string& nm = p.gp->buf_names[static_cast<size_t>(b)];
+      auto it = std::find(gw.buffers.begin(), gw.buffers.end(), nm);
+      if (it == gw.buffers.end()) return false;
+      size_t i = static_cast<size_t>(it - gw.buffers.begin());
+      B->ptr[b] = gbuf[i];
+      B->dtype[b] = gbuf_dtype[i];
+      for (int d = 0; d < g.ndim[b]; ++d) B->shape[b][d] = g.shape[b][d];
+    }
+    return true;
+  }
+
+  bool launch_general(const Plan& p, const unsigned long long* dl, int* flag) {
+    GenBuffers B;
+    if (!general_buffers(p, &B)) return false;
+    for (const GStep& stp : p.gp->steps) {
+      GenBlock g = p.gp->gen.blocks[static_cast<size_t>(stp.block)];
+      bool ok = true;
+      if (stp.family == F_SIMTA) {
+        ok = launch_simta(B.ptr[stp.x_buf], B.ptr[stp.y_buf], static_cast<float*>(B.ptr[stp.c_buf]), stp.aff, bf16, dl,
+                          flag, st);
+      } else if (stp.family == F_NESTGEN) {
+        ok = launch_generic_nest(g, p.gcode, B, dl, flag, st);
+      } else {
+        if (stp.epilogue_pass) {  // rewrite the accumulated element through the epilogue
+          for (int i = 0; i < g.nl; ++i)
+            if ((g.red_mask >> i) & 1u) g.ext[i] = 1;
+          g.red_mask = 0;
+          g.red_trip = 1;
+          g.value_code = g.epi_code;
+          g.init_code = -1;
+          g.epi_code = -1;
+        }
+        ok = launch_generic_block(g, p.gcode, B, false, dl, flag, st);
+      }
+      if (!ok) return false;
+    }
+    return true;
+  }
 
   bool launch(const Plan& p, bool guarded, int slot) {
     const unsigned long long* dl = guarded ? deadline : nullptr;
     int* flag = flags + slot;
+    if (p.gp) {
+      launches += static_cast<int64_t>(p.gp->steps.size());
+      return launch_general(p, dl, flag);
+    }
     const size_t cbytes = static_cast<size_t>(w.c_elems) * sizeof(float);
     if (p.needs_zero && cudaMemsetAsync(c, 0, cbytes, st) != cudaSuccess) return false;
     ++launches;
@@ -201,8 +264,8 @@ struct ls_runner {
 
 namespace {
 
-ls_status plan_all(const Workload& w, const DeviceLimits& lim, const char* const* programs, const size_t* lens, int n,
-                   std::vector<Plan>* plans) {
+ls_status plan_all(const Workload& w, const GeneralWorkload* gw, const DeviceLimits& lim,
+                   const char* const* programs, const size_t* lens, int n, std::vector<Plan>* plans) {
   plans->assign(static_cast<size_t>(n), Plan());
   parallel_for(n, [&](int i) {
     std::string err;
@@ -213,8 +276,111 @@ ls_status plan_all(const Workload& w, const DeviceLimits& lim, const char* const
       out.why = err;
       return;
     }
+    if (gw) {
+      auto g = std::make_shared<GeneralPlan>(plan_general(*gw, *p, lim));
+      out.status = g->status;
+      out.why = g->why;
+      out.family = g->family;
+      std::memcpy(out.cfg, g->cfg, sizeof out.cfg);
+      out.gp = g;
+      return;
+    }
     out = plan_program(w, *p, lim);
   });
+  return LS_OK;
+}
+
+
+// General workload: device buffers for every e0 buffer, reference output by
+// the generic executor in fp64 (intermediates in fp64 too).
+ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWorkload& gw, const std::string& text,
+                               const float* const* host_inputs, int n_inputs) {
+  int ninp = 0;
+  for (int role : gw.roles) ninp += role == 0;
+  if (ninp != n_inputs) {
+    set_error("ls_runner_set_workload: input count does not match the program's input buffers");
+    return LS_ERR_ARG;
+  }
+  GenProgram gen;
+  std::string err;
+  if (!encode_generic(e0, &gen, &err)) {
+    set_error("e0: " + err);
+    return LS_ERR_ARG;
+  }
+  r->gw = gw;
+  r->general = true;
+  r->e0_text = text;
+  r->w = Workload();
+  r->w.c_elems = gw.c_elems;
+  const size_t nb = gw.buffers.size();
+  r->gbuf.assign(nb, nullptr);
+  r->gbuf_dtype.assign(nb, r->bf16 ? 0 : 1);
+  std::vector<void*> refbuf(nb, nullptr);
+  std::vector<int> refdt(nb, 2);
+  const size_t es = r->bf16 ? 2 : 4;
+  int inp = 0;
+  std::vector<void*> temps;
+  for (size_t b = 0; b < nb; ++b) {
+    int64_t elems = 1;
+    for (int64_t x : gw.shapes[b]) elems *= x;
+    const size_t n = static_cast<size_t>(elems);
+    if (gw.roles[b] == 0) {  // input: runner dtype, shared by the reference run
+      LSB_CUDA(cudaMalloc(&r->gbuf[b], n * es));
+      if (r->bf16) {
+        float* tmp = nullptr;
+        LSB_CUDA(cudaMalloc(&tmp, n * 4));
+        LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[inp], n * 4, cudaMemcpyHostToDevice, r->st));
+        launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(r->gbuf[b]), elems, r->st);
+        LSB_CUDA(cudaStreamSynchronize(r->st));
+        cudaFree(tmp);
+      } else {
+        LSB_CUDA(cudaMemcpyAsync(r->gbuf[b], host_inputs[inp], n * 4, cudaMemcpyHostToDevice, r->st));
+      }
+      ++inp;
+      refbuf[b] = r->gbuf[b];
+      refdt[b] = r->gbuf_dtype[b];
+    } else if (gw.roles[b] == 1 && gw.buffers[b] == gw.c_buf) {  // contraction output
+      LSB_CUDA(cudaMalloc(&r->c, n * 4));
+      LSB_CUDA(cudaMalloc(&r->ref, n * 8));
+      r->gbuf[b] = r->c;
+      r->gbuf_dtype[b] = 1;
+      refbuf[b] = r->ref;
+    } else if (gw.roles[b] == 1) {  // the final output of a later stage (e.g. relu)
+      LSB_CUDA(cudaMalloc(&r->c, n * 4));
+      LSB_CUDA(cudaMalloc(&r->ref, n * 8));
+      r->gbuf[b] = r->c;
+      r->gbuf_dtype[b] = 1;
+      r->w.c_elems = elems;
+      refbuf[b] = r->ref;
+    } else {  // intermediate: fp32 when it holds the contraction's sums, else runner dtype
+      if (gw.buffers[b] == gw.c_buf) r->gbuf_dtype[b] = 1;
+      LSB_CUDA(cudaMalloc(&r->gbuf[b], n * (r->gbuf_dtype[b] == 1 ? 4 : es)));
+      LSB_CUDA(cudaMalloc(&refbuf[b], n * 8));
+      temps.push_back(refbuf[b]);
+    }
+  }
+  // reference output: e0 block by block in fp64
+  int64_t* code = nullptr;
+  LSB_CUDA(cudaMalloc(&code, std::max<size_t>(gen.code.size(), 1) * 8));
+  LSB_CUDA(cudaMemcpyAsync(code, gen.code.data(), gen.code.size() * 8, cudaMemcpyHostToDevice, r->st));
+  GenBuffers B;
+  std::memset(&B, 0, sizeof B);
+  for (size_t b = 0; b < nb; ++b) {
+    B.ptr[b] = refbuf[b];
+    B.dtype[b] = refdt[b];
+    for (int d = 0; d < gen.ndim[b]; ++d) B.shape[b][d] = gen.shape[b][d];
+  }
+  for (const GenBlock& g : gen.blocks)
+    if (!launch_generic_block(g, code, B, true, nullptr, nullptr, r->st)) {
+      set_error("reference run of e0 failed to launch");
+      return LS_ERR_CUDA;
+    }
+  LSB_CUDA(cudaStreamSynchronize(r->st));
+  cudaFree(code);
+  for (void* t : temps) cudaFree(t);
+  r->tc_ok = false;
+  r->lim.bf16 = false;
+  r->have_workload = true;
   return LS_OK;
 }
 
@@ -235,14 +401,20 @@ ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* pro
     return LS_ERR_PARSE;
   }
   Workload w;
+  GeneralWorkload gw;
+  bool general = false;
   if (!analyze_workload(*p0, &w, &err)) {
-    set_error("e0: " + err);
-    return LS_ERR_ARG;
+    std::string err2;
+    if (!analyze_general(*p0, &gw, &err2)) {
+      set_error("e0: " + err + "; " + err2);
+      return LS_ERR_ARG;
+    }
+    general = true;
   }
   DeviceLimits lim;
-  lim.bf16 = dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
+  lim.bf16 = !general && dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
   std::vector<Plan> plans;
-  plan_all(w, lim, programs, lens, n, &plans);
+  plan_all(w, general ? &gw : nullptr, lim, programs, lens, n, &plans);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   return LS_OK;
 }
@@ -313,8 +485,13 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
   }
   Workload w;
   if (!analyze_workload(*p0, &w, &err)) {
-    set_error("e0: " + err);
-    return LS_ERR_ARG;
+    GeneralWorkload gw;
+    std::string err2;
+    if (!analyze_general(*p0, &gw, &err2)) {
+      set_error("e0: " + err + "; " + err2);
+      return LS_ERR_ARG;
+    }
+    return set_general_workload(r, *p0, gw, std::string(e0, len), host_inputs, n_inputs);
   }
   if (static_cast<int>(w.input_bufs.size()) != n_inputs) {
     set_error("ls_runner_set_workload: input count does not match the program's input buffers");
@@ -394,7 +571,7 @@ ls_status ls_runner_plan(ls_runner* r, const char* const* programs, const size_t
     return LS_ERR_STATE;
   }
   std::vector<Plan> plans;
-  plan_all(r->w, r->lim, programs, lens, n, &plans);
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   return LS_OK;
 }
@@ -412,9 +589,28 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   ls_status s = r->ensure_capacity(n);
   if (s != LS_OK) return s;
   std::vector<Plan> plans;
-  plan_all(r->w, r->lim, programs, lens, n, &plans);
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   r->launches = 0;
+  if (r->general) {  // one upload of every candidate's bytecode
+    std::vector<int64_t> all;
+    std::vector<size_t> at(static_cast<size_t>(n), 0);
+    for (int i = 0; i < n; ++i) {
+      const Plan& p = plans[static_cast<size_t>(i)];
+      if (p.status != P_OK || !p.gp) continue;
+      at[static_cast<size_t>(i)] = all.size();
+      all.insert(all.end(), p.gp->gen.code.begin(), p.gp->gen.code.end());
+    }
+    if (all.size() > r->gcode_cap) {
+      cudaFree(r->gcode);
+      r->gcode = nullptr;
+      r->gcode_cap = std::max(all.size(), 2 * r->gcode_cap);
+      LSB_CUDA(cudaMalloc(&r->gcode, r->gcode_cap * 8));
+    }
+    if (!all.empty()) LSB_CUDA(cudaMemcpyAsync(r->gcode, all.data(), all.size() * 8, cudaMemcpyHostToDevice, r->st));
+    for (int i = 0; i < n; ++i)
+      if (plans[static_cast<size_t>(i)].gp) plans[static_cast<size_t>(i)].gcode = r->gcode + at[static_cast<size_t>(i)];
+  }
   const size_t cbytes = static_cast<size_t>(r->w.c_elems) * sizeof(float);
   const unsigned long long timeout_ns = static_cast<unsigned long long>(r->opts.timeout_ms * 1e6);
   LSB_CUDA(cudaMemsetAsync(r->flags, 0, static_cast<size_t>(n) * sizeof(int), r->st));
@@ -441,11 +637,19 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   // best-so-far (and with it every later deadline) drops early; results are
   // still reported in candidate order
   std::vector<int> order;
-  for (int pass = 0; pass < 4; ++pass) {
-    static const int fam_order[4] = {F_TC, F_SIMT, F_NAIVE, F_LOOPNEST};
-    for (int i = 0; i < n; ++i)
-      if (plans[static_cast<size_t>(i)].status == P_OK && plans[static_cast<size_t>(i)].family == fam_order[pass])
-        order.push_back(i);
+  {
+    auto rank = [](int fam) {
+      switch (fam) {
+        case F_TC: return 0;
+        case F_SIMT: case F_SIMTA: return 1;
+        case F_NAIVE: case F_GENERIC: return 2;
+        default: return 3;  // LOOPNEST, NESTGEN
+      }
+    };
+    for (int pass = 0; pass < 4; ++pass)
+      for (int i = 0; i < n; ++i)
+        if (plans[static_cast<size_t>(i)].status == P_OK && rank(plans[static_cast<size_t>(i)].family) == pass)
+          order.push_back(i);
   }
   int prev = -1;
   for (int i : order) {
@@ -473,6 +677,8 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     set_error(std::string("runner phase A: ") + cudaGetErrorString(se));
     return LS_ERR_CUDA;
   }
+  for (int i = 0; i < n; ++i)
+    if (out[i].status == LS_RUN_OK && !launched[static_cast<size_t>(i)]) out[i].status = LS_RUN_LAUNCH;
   std::vector<int> tflag(static_cast<size_t>(n));
   std::vector<unsigned long long> par(static_cast<size_t>(2 * n));
   LSB_CUDA(cudaMemcpy(tflag.data(), r->flags, static_cast<size_t>(n) * sizeof(int), cudaMemcpyDeviceToHost));

@@ -1,0 +1,185 @@
+// SIMT-A: affine SIMT tile kernel for multi-axis contractions (implicit GEMM).
+// Included by simta_f32.cu / simta_bf16.cu (one dtype each, compiled in
+// parallel).  See affine.hpp for the mapping convention.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "affine.hpp"
+#include "simta.cuh"
+
+namespace lsb {
+namespace simta {
+
+__device__ __forceinline__ float ld1(const float* p, int64_t i) { return __ldg(p + i); }
+__device__ __forceinline__ float ld1(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// digits of idx over the parts of one list (nest order, last fastest)
+__device__ __forceinline__ void decode(const AList& L, int64_t idx, int64_t* sx, int64_t* sy, int64_t* sc,
+                                       int64_t* g0, int64_t* g1) {
+  for (int p = L.n - 1; p >= 0; --p) {
+    const int64_t d = idx % L.ext[p];
+    idx /= L.ext[p];
+    *sx += d * L.cx[p];
+    *sy += d * L.cy[p];
+    *sc += d * L.cc[p];
+    *g0 += d * L.cg0[p];
+    *g1 += d * L.cg1[p];
+  }
+}
+
+template <typename T, int RM, int RN>
+__global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, const T* __restrict__ y,
+                                                     float* __restrict__ c, SimtaArgs a) {
+  extern __shared__ float sm[];
+  __shared__ int abort_flag;
+  const int tid = threadIdx.x;
+  const int tn = (int)a.tn, tm = (int)a.tm, nthr = tm * tn;
+  const int tn_i = tid % tn, tm_i = tid / tn;
+  const int bm = tm * RM, bn = tn * RN, bk = (int)a.bk;
+  const int lda = bm + 1, ldb = bn + 1;
+  float* As = sm;
+  float* Bs = As + bk * lda;
+  int* offXM = reinterpret_cast<int*>(Bs + bk * ldb);
+  int* offCM = offXM + bm;
+  int* offYN = offCM + bm;
+  int* offCN = offYN + bn;
+  int* offXK = offCN + bn;
+  int* offYK = offXK + bk;
+  int* gM0 = offYK + bk;
+  int* gM1 = gM0 + bm;
+  int* gK0 = gM1 + bm;
+  int* gK1 = gK0 + bk;
+
+  // ---- per-CTA address tables ----
+  for (int mm = tid; mm < bm; mm += nthr) {
+    int64_t sx = 0, sy = 0, sc = 0, g0 = 0, g1 = 0;
+    decode(a.m_thr, mm / RM, &sx, &sy, &sc, &g0, &g1);
+    decode(a.m_reg, mm % RM, &sx, &sy, &sc, &g0, &g1);
+    offXM[mm] = (int)sx; offCM[mm] = (int)sc; gM0[mm] = (int)g0; gM1[mm] = (int)g1;
+  }
+  for (int nn = tid; nn < bn; nn += nthr) {
+    int64_t sx = 0, sy = 0, sc = 0, g0 = 0, g1 = 0;
+    decode(a.n_thr, nn / RN, &sx, &sy, &sc, &g0, &g1);
+    decode(a.n_reg, nn % RN, &sx, &sy, &sc, &g0, &g1);
+    offYN[nn] = (int)sy; offCN[nn] = (int)sc;
+  }
+  for (int kk = tid; kk < bk; kk += nthr) {
+    int64_t sx = 0, sy = 0, sc = 0, g0 = 0, g1 = 0;
+    decode(a.k_bk, kk, &sx, &sy, &sc, &g0, &g1);
+    offXK[kk] = (int)sx; offYK[kk] = (int)sy; gK0[kk] = (int)g0; gK1[kk] = (int)g1;
+  }
+  int64_t bx = a.x0, by = a.y0, bc = a.c0, bg0 = a.g0[0], bg1 = a.g0[1];
+  decode(a.m_grid, blockIdx.y, &bx, &by, &bc, &bg0, &bg1);
+  decode(a.n_grid, blockIdx.x, &bx, &by, &bc, &bg0, &bg1);
+  __syncthreads();
+
+  float acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
+
+  for (int64_t kt = 0; kt < a.kt; ++kt) {
+    if (a.deadline) {
+      if (tid == 0) abort_flag = gtimer() > *a.deadline;
+      __syncthreads();
+      if (abort_flag) {
+        if (tid == 0) atomicExch(a.timed_out, 1);
+        return;
+      }
+    }
+    int64_t kx = bx, ky = by, kc = 0, kg0 = bg0, kg1 = bg1;
+    decode(a.k_tile, kt, &kx, &ky, &kc, &kg0, &kg1);
+    // A tile (k fastest: consecutive threads walk k)
+    for (int e = tid; e < bm * bk; e += nthr) {
+      const int kk = e % bk, mm = e / bk;
+      float v = 0.f;
+      bool ok = true;
+      if (a.ng > 0) {
+        const int64_t h = kg0 + gM0[mm] + gK0[kk];
+        ok = h >= 0 && h < a.gext[0];
+        if (a.ng > 1) {
+          const int64_t w2 = kg1 + gM1[mm] + gK1[kk];
+          ok = ok && w2 >= 0 && w2 < a.gext[1];
+        }
+      }
+      if (ok) v = ld1(x, kx + offXM[mm] + offXK[kk]);
+      As[kk * lda + mm] = v;
+    }
+    for (int e = tid; e < bn * bk; e += nthr) {
+      const int nn = e % bn, kk = e / bn;
+      Bs[kk * ldb + nn] = ld1(y, ky + offYN[nn] + offYK[kk]);
+    }
+    __syncthreads();
+    const float* Ap = As + tm_i * RM;
+    const float* Bp = Bs + tn_i * RN;
+#pragma unroll 4
+    for (int kk = 0; kk < bk; ++kk) {
+      float av[RM], bv[RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i) av[i] = Ap[kk * lda + i];
+#pragma unroll
+      for (int j = 0; j < RN; ++j) bv[j] = Bp[kk * ldb + j];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) c[bc + offCM[tm_i * RM + i] + offCN[tn_i * RN + j]] = acc[i][j];
+}
+
+template <typename T, int RM, int RN>
+cudaError_t launch_one(const void* x, const void* y, float* c, const SimtaArgs& a, size_t smem, cudaStream_t st) {
+  auto fn = simta_kernel<T, RM, RN>;
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(fn));
+    if (max_dyn <= 0) return cudaErrorInvalidValue;
+  }
+  if (smem > static_cast<size_t>(max_dyn)) return cudaErrorInvalidValue;
+  dim3 grid(static_cast<unsigned>(a.gn), static_cast<unsigned>(a.gm), 1);
+  fn<<<grid, static_cast<unsigned>(a.tm * a.tn), smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(y), c, a);
+  return cudaGetLastError();
+}
+
+typedef cudaError_t (*Launcher)(const void*, const void*, float*, const SimtaArgs&, size_t, cudaStream_t);
+
+template <typename T, int RM>
+void row(Launcher* r) {
+  r[0] = launch_one<T, RM, 1>;
+  r[1] = launch_one<T, RM, 2>;
+  r[2] = RM * 3 <= 64 ? launch_one<T, RM, 3> : nullptr;
+  r[3] = RM * 4 <= 64 ? launch_one<T, RM, 4> : nullptr;
+  r[4] = RM * 6 <= 64 ? launch_one<T, RM, 6> : nullptr;
+  r[5] = RM * 7 <= 64 ? launch_one<T, RM, 7> : nullptr;
+  r[6] = RM * 8 <= 64 ? launch_one<T, RM, 8> : nullptr;
+  r[7] = RM * 12 <= 64 ? launch_one<T, RM, 12> : nullptr;
+  r[8] = RM * 14 <= 64 ? launch_one<T, RM, 14> : nullptr;
+  r[9] = RM * 16 <= 64 ? launch_one<T, RM, 16> : nullptr;
+}
+
+template <typename T>
+struct Table {
+  Launcher t[10][10];
+  Table() {
+    row<T, 1>(t[0]); row<T, 2>(t[1]); row<T, 3>(t[2]); row<T, 4>(t[3]); row<T, 6>(t[4]);
+    row<T, 7>(t[5]); row<T, 8>(t[6]); row<T, 12>(t[7]); row<T, 14>(t[8]); row<T, 16>(t[9]);
+  }
+};
+
+}  // namespace simta
+}  // namespace lsb

@@ -163,3 +163,54 @@ def test_measure_signature_matches_reference_runner():
     assert len(out) == 8 and all(isinstance(x, Fraction) and x > 0 for x in out)
     assert isinstance(r.baseline(), Fraction)
     r.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_conv2d_general_path_bit_exact(dtype):
+    """conv2d NHWC (pad stage + implicit GEMM): the fp64 reference run equals
+    the numpy oracle; SIMT-A (pad stage separate and pad inlined as a guarded
+    load), nest-generic and the unscheduled e0 match it bit-exactly."""
+    import json
+    hdr, pop = load_population("conv2d")
+    e0 = hdr["e0"]
+    r = make_runner(dtype, timeout_ms=200.0)
+    r.set_workload(e0, seed=0)
+    want = O.reference_outputs(e0, random_inputs(e0, 0))["O"]
+    assert np.array_equal(r.reference_output(), want)
+    progs = [p["program"] for p in pop]
+    plans = r.plan_programs(progs)
+    inlined = [i for i, p in enumerate(progs)
+               if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
+    picks = pick(plans, "simt_affine", 6) + inlined[:4] + pick(plans, "nestgen", 1)
+    assert picks
+    for i in picks:
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] in ("OK", "TIMEOUT"), res
+        if res["status"] == "OK":
+            assert res["mismatches"] == 0, res
+            assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
+    base = r.baseline_result()
+    assert base["status"] == "OK" and base["mismatches"] == 0
+    r.close()
+
+
+def test_dense_relu_general_path_exact():
+    from paper_2205_13603_b200.inputs import random_inputs as ri
+    import gzip
+    import json
+    import os
+    from conftest import GOLDEN
+    rows = [json.loads(l) for l in open(os.path.join(GOLDEN, "programs.jsonl"))]
+    progs = [x["program"] for x in rows if x["name"].startswith("dense_relu")]
+    e0 = next(x["program"] for x in rows if x["name"] == "dense_relu_e0")
+    r = make_runner("bf16", timeout_ms=200.0)
+    r.set_workload(e0, seed=3)
+    want = O.reference_outputs(e0, ri(e0, 3))["R"]
+    assert np.array_equal(r.reference_output(), want)
+    res = r.measure_programs(progs)
+    ok = [x for x in res if x["status"] == "OK"]
+    assert ok
+    for x in res:
+        if x["status"] == "OK":
+            assert x["mismatches"] == 0, x
+    r.close()

@@ -66,9 +66,26 @@ def test_bmm_batch_axis_mapping():
 
 
 def test_unsupported_workload_is_reported():
+    # an elementwise-only program has no contraction for the runner to time
+    relu = ('{"buffers": [{"name": "A", "role": "input", "shape": [8]}, {"name": "B", "role": "output", '
+            '"shape": [8]}], "root": [{"loop": {"body": [{"compute": {"buffer": "B", "indices": [{"var": "i"}], '
+            '"name": "relu", "value": {"max": [{"load": {"buffer": "A", "indices": [{"var": "i"}]}}, {"int": 0}]}}}], '
+            '"extent": 8, "kind": "serial", "var": "i"}}]}')
+    with pytest.raises(native.NativeError, match="no contraction block"):
+        plan(relu, [relu])
+
+
+def test_conv2d_general_families():
     hdr, pop = load_population("conv2d")
-    with pytest.raises(native.NativeError, match="single-block"):
-        plan(hdr["e0"], [pop[0]["program"]])
+    res = plan(hdr["e0"], [p["program"] for p in pop])
+    fams = Counter((r["family"], r["status"]) for r in res)
+    assert fams[("simt_affine", "OK")] > 100 and fams[("nestgen", "OK")] > 0
+    for r in res:
+        if r["family"] == "simt_affine":
+            gb, gm, gn, tb, tm, tn, rb, rm, rn, bk, kt = r["cfg"][:11]
+            assert gm * tm * rm == 56 * 56 and gn * tn * rn == 64 and bk * kt == 3 * 3 * 64
+    e0r, = plan(hdr["e0"], [hdr["e0"]])
+    assert (e0r["family"], e0r["status"]) == ("naive", "OK")
 
 
 def test_parse_errors_are_per_candidate():
