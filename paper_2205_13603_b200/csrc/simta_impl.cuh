@@ -99,25 +99,39 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
     }
     int64_t kx = bx, ky = by, kc = 0, kg0 = bg0, kg1 = bg1;
     decode(a.k_tile, kt, &kx, &ky, &kc, &kg0, &kg1);
-    // A tile (k fastest: consecutive threads walk k)
-    for (int e = tid; e < bm * bk; e += nthr) {
-      const int kk = e % bk, mm = e / bk;
-      float v = 0.f;
-      bool ok = true;
-      if (a.ng > 0) {
-        const int64_t h = kg0 + gM0[mm] + gK0[kk];
-        ok = h >= 0 && h < a.gext[0];
-        if (a.ng > 1) {
-          const int64_t w2 = kg1 + gM1[mm] + gK1[kk];
-          ok = ok && w2 >= 0 && w2 < a.gext[1];
+    // A tile, k fastest (consecutive threads walk the contiguous ci axis);
+    // carried (mm, kk) indices: no per-element division
+    {
+      int kk = tid % bk, mm = tid / bk;
+      const int skk = nthr % bk, smm = nthr / bk;
+      for (int e = tid; e < bm * bk; e += nthr) {
+        float v = 0.f;
+        bool ok = true;
+        if (a.ng > 0) {
+          const int64_t h = kg0 + gM0[mm] + gK0[kk];
+          ok = h >= 0 && h < a.gext[0];
+          if (a.ng > 1) {
+            const int64_t w2 = kg1 + gM1[mm] + gK1[kk];
+            ok = ok && w2 >= 0 && w2 < a.gext[1];
+          }
         }
+        if (ok) v = ld1(x, kx + offXM[mm] + offXK[kk]);
+        As[kk * lda + mm] = v;
+        kk += skk;
+        mm += smm;
+        if (kk >= bk) { kk -= bk; ++mm; }
       }
-      if (ok) v = ld1(x, kx + offXM[mm] + offXK[kk]);
-      As[kk * lda + mm] = v;
     }
-    for (int e = tid; e < bn * bk; e += nthr) {
-      const int nn = e % bn, kk = e / bn;
-      Bs[kk * ldb + nn] = ld1(y, ky + offYN[nn] + offYK[kk]);
+    // B tile, n fastest (co is contiguous in HWIO weights)
+    {
+      int nn = tid % bn, kk = tid / bn;
+      const int snn = nthr % bn, skk = nthr / bn;
+      for (int e = tid; e < bn * bk; e += nthr) {
+        Bs[kk * ldb + nn] = ld1(y, ky + offYN[nn] + offYK[kk]);
+        nn += snn;
+        kk += skk;
+        if (nn >= bn) { nn -= bn; ++kk; }
+      }
     }
     __syncthreads();
     const float* Ap = As + tm_i * RM;
