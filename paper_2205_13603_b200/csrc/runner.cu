@@ -704,41 +704,70 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
 
   r->stats[0] = host_now() - h0;
   h0 = host_now();
-  // ---- phase B: timed repeats, chunked behind a device spin ----
+  // ---- phase B: timed repeats ----
+  // Each candidate's repeats are captured into one CUDA graph (PDL edges
+  // between tcgen05 launches are preserved) and the graph launch is
+  // bracketed by two events, so no host launch gap can enter the timing.
+  // If capture fails the repeats are launched directly behind a device spin
+  // sized to the host enqueue time.
   std::vector<int> reps(static_cast<size_t>(n), 0);
+  std::vector<cudaGraphExec_t> execs;
   const int chunk = 32;
   double prev_gpu_us = 0.0;
   for (int c0 = 0; c0 < n; c0 += chunk) {
     int c1 = std::min(n, c0 + chunk);
-    int64_t calls = 0;
+    std::vector<cudaGraphExec_t> ge(static_cast<size_t>(c1 - c0), nullptr);
+    int64_t direct_calls = 0;
     double gpu_us = 0.0;
     for (int i = c0; i < c1; ++i) {
       if (!launched[static_cast<size_t>(i)]) continue;
+      const Plan& p = plans[static_cast<size_t>(i)];
       double wm = std::max(1e-4, static_cast<double>(warm[static_cast<size_t>(i)]));
       int rep = static_cast<int>(std::ceil(r->opts.target_ms / wm));
       rep = std::max(r->opts.min_repeats, std::min(r->opts.max_repeats, rep));
       reps[static_cast<size_t>(i)] = rep;
-      calls += rep * (plans[static_cast<size_t>(i)].needs_zero ? 2 : 1) + 2;
       gpu_us += rep * wm * 1e3;
+      // graphs only where launch gaps could matter: fast candidates (the
+      // instantiation costs ~0.1 ms of host time per candidate)
+      if (r->opts.flush_l2 == 0 && wm < 0.02) {
+        cudaGraph_t g = nullptr;
+        bool ok = cudaStreamBeginCapture(r->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        for (int k = 0; ok && k < rep; ++k) ok = r->launch(p, false, i);
+        cudaError_t ce = cudaStreamEndCapture(r->st, &g);
+        ok = ok && ce == cudaSuccess && g &&
+             cudaGraphInstantiate(&ge[static_cast<size_t>(i - c0)], g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {
+          cudaGetLastError();
+          ge[static_cast<size_t>(i - c0)] = nullptr;
+        }
+      }
+      if (!ge[static_cast<size_t>(i - c0)]) direct_calls += rep * (p.needs_zero ? 2 : 1) + 2;
     }
-    if (!calls) continue;
-    double host_us = r->launch_host_us * static_cast<double>(calls);
-    double spin = host_us - prev_gpu_us;
-    if (spin > 0) {
-      r->stats[2] += std::min(spin, 20000.0);
-      launch_delay(static_cast<unsigned long long>(std::min(spin, 20000.0) * 1e3), r->st);
-      ++r->launches;
+    if (direct_calls) {
+      double spin = r->launch_host_us * static_cast<double>(direct_calls) - prev_gpu_us;
+      if (spin > 0) {
+        r->stats[2] += std::min(spin, 20000.0);
+        launch_delay(static_cast<unsigned long long>(std::min(spin, 20000.0) * 1e3), r->st);
+        ++r->launches;
+      }
     }
     for (int i = c0; i < c1; ++i) {
       if (!launched[static_cast<size_t>(i)]) continue;
       const Plan& p = plans[static_cast<size_t>(i)];
+      cudaGraphExec_t g = ge[static_cast<size_t>(i - c0)];
       LSB_CUDA(cudaEventRecord(E[4 * i + 2], r->st));
-      for (int k = 0; k < reps[static_cast<size_t>(i)]; ++k)
-        if (!r->launch(p, false, i)) {
-          set_error("runner phase B: launch failed");
-          cudaEventDestroy(batch0);
-          return LS_ERR_CUDA;
-        }
+      if (g) {
+        LSB_CUDA(cudaGraphLaunch(g, r->st));
+        execs.push_back(g);
+      } else {
+        for (int k = 0; k < reps[static_cast<size_t>(i)]; ++k)
+          if (!r->launch(p, false, i)) {
+            set_error("runner phase B: launch failed");
+            cudaEventDestroy(batch0);
+            return LS_ERR_CUDA;
+          }
+      }
       LSB_CUDA(cudaEventRecord(E[4 * i + 3], r->st));
     }
     prev_gpu_us = gpu_us;
@@ -748,6 +777,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   LSB_CUDA(cudaEventCreate(&batch1));
   LSB_CUDA(cudaEventRecord(batch1, r->st));
   se = cudaStreamSynchronize(r->st);
+  for (cudaGraphExec_t g : execs) cudaGraphExecDestroy(g);
   if (se != cudaSuccess) {
     set_error(std::string("runner phase B: ") + cudaGetErrorString(se));
     return LS_ERR_CUDA;
