@@ -112,7 +112,7 @@ enum {
 
 /* kernel families */
 enum { LS_FAM_NONE = 0, LS_FAM_NAIVE = 1, LS_FAM_SIMT = 2, LS_FAM_TCGEN05 = 3, LS_FAM_LOOPNEST = 4,
-       LS_FAM_GENERIC = 5, LS_FAM_NESTGEN = 6, LS_FAM_SIMT_AFFINE = 7 };
+       LS_FAM_GENERIC = 5, LS_FAM_NESTGEN = 6, LS_FAM_SIMT_AFFINE = 7, LS_FAM_TCGEN05_CONV = 8 };
 
 typedef struct {
   int32_t status;

@@ -143,6 +143,136 @@ bool analyze_general(const Program& e0, GeneralWorkload* w, std::string* err) {
   return true;
 }
 
+namespace {
+
+struct LoopPart { int axis; int64_t ext, stride; Kind kind; int var; };
+
+// Recognise the tcgen05 conv structure and fill its configuration.
+bool tc_conv_plan(const GeneralWorkload& w, const Program& p, const Stmt* s, const Expr* xl, const Expr* yl,
+                  const std::vector<LoopPart>& lps, bool guarded, const DeviceLimits& lim, TcConvCfg* out) {
+  (void)guarded;
+  if (xl->kids.size() != 4 || lps.size() < 4) return false;
+  const size_t nv = p.vars.size();
+  // per X dim affine coefficients (n, h, w, c)
+  std::vector<int64_t> xd[4];
+  int64_t x0[4];
+  for (int d = 0; d < 4; ++d)
+    if (!affine_coeffs(xl->kids[static_cast<size_t>(d)], nv, &xd[d], &x0[d])) return false;
+  // merge adjacent parts of one axis (innermost coefficients describe the merged loop)
+  struct MP { int axis, group; int64_t ext; int var; };
+  std::vector<MP> mp;
+  for (const LoopPart& q : lps) {
+    int g = w.axis_group[static_cast<size_t>(q.axis)];
+    if (!mp.empty() && mp.back().axis == q.axis) { mp.back().ext *= q.ext; mp.back().var = q.var; }
+    else mp.push_back(MP{q.axis, g, q.ext, q.var});
+  }
+  const size_t m = mp.size();
+  if (m < 4) return false;
+  const MP &ph = mp[m - 4], &pw = mp[m - 3], &pn = mp[m - 2], &pk = mp[m - 1];
+  auto co = [&](int d, int var) { return xd[d][static_cast<size_t>(var)]; };
+  if (ph.group != AG_M || pw.group != AG_M || pn.group != AG_N || pk.group != AG_K) return false;
+  if (ph.ext != 8 || pw.ext != 8 || pk.ext != 64 || pn.ext % 16 != 0) return false;
+  if (co(1, ph.var) != 1 || co(0, ph.var) || co(2, ph.var) || co(3, ph.var)) return false;
+  if (co(2, pw.var) != 1 || co(0, pw.var) || co(1, pw.var) || co(3, pw.var)) return false;
+  if (co(3, pk.var) != 1 || co(0, pk.var) || co(1, pk.var) || co(2, pk.var)) return false;
+  // Y: N must be the last (contiguous) dim of the weight so a K-major copy exists
+  const Buffer& YB = p.buffers[static_cast<size_t>(yl->buffer)];
+  const int64_t ncols = YB.shape.back();
+  std::vector<int64_t> ystr(YB.shape.size(), 1);
+  for (size_t d = YB.shape.size(); d-- > 1;) ystr[d - 1] = ystr[d] * YB.shape[d];
+  std::vector<int64_t> cy(nv, 0), cc(nv, 0);
+  int64_t y0 = 0, c0 = 0;
+  for (size_t d = 0; d < yl->kids.size(); ++d) {
+    std::vector<int64_t> c;
+    int64_t k0;
+    if (!affine_coeffs(yl->kids[d], nv, &c, &k0)) return false;
+    for (size_t x = 0; x < nv; ++x) cy[x] += ystr[d] * c[x];
+    y0 += ystr[d] * k0;
+  }
+  const Buffer& CB = p.buffers[static_cast<size_t>(s->buffer)];
+  std::vector<int64_t> cstr(CB.shape.size(), 1);
+  for (size_t d = CB.shape.size(); d-- > 1;) cstr[d - 1] = cstr[d] * CB.shape[d];
+  for (size_t d = 0; d < s->indices.size(); ++d) {
+    std::vector<int64_t> c;
+    int64_t k0;
+    if (!affine_coeffs(s->indices[d], nv, &c, &k0)) return false;
+    for (size_t x = 0; x < nv; ++x) cc[x] += cstr[d] * c[x];
+    c0 += cstr[d] * k0;
+  }
+  if (y0 != 0 || cy[static_cast<size_t>(pn.var)] != 1 || cc[static_cast<size_t>(pn.var)] != 1) return false;
+  if (cy[static_cast<size_t>(pk.var)] != ncols || cc[static_cast<size_t>(pk.var)] != 0) return false;
+  if (cy[static_cast<size_t>(ph.var)] || cy[static_cast<size_t>(pw.var)]) return false;
+  for (int d = 0; d < 4; ++d)
+    if (co(d, pn.var)) return false;
+  TcConvCfg& t = *out;
+  std::memset(&t, 0, sizeof t);
+  t.x_n0 = x0[0]; t.x_h0 = x0[1]; t.x_w0 = x0[2]; t.x_c0 = x0[3];
+  t.c0 = c0;
+  t.cc_h1 = cc[static_cast<size_t>(ph.var)];
+  t.cc_w1 = cc[static_cast<size_t>(pw.var)];
+  t.bn = pn.ext;
+  t.splits = t.kt = t.grid_m = t.grid_n = 1;
+  bool before_spatial = true;
+  // outer loops (everything but the four innermost merged parts)
+  size_t outer_loops = lps.size();
+  {
+    // count loops belonging to the innermost 4 merged parts
+    size_t inner = 0;
+    int last_axis = -1;
+    int merged = 0;
+    for (size_t i = lps.size(); i-- > 0;) {
+      if (lps[i].axis != last_axis) { ++merged; last_axis = lps[i].axis; }
+      if (merged > 4) break;
+      ++inner;
+    }
+    outer_loops = lps.size() - inner;
+  }
+  for (size_t i = 0; i < outer_loops; ++i) {
+    const LoopPart& q = lps[i];
+    const size_t v = static_cast<size_t>(q.var);
+    int g = w.axis_group[static_cast<size_t>(q.axis)];
+    CList* L;
+    if (g == AG_K) {
+      L = before_spatial ? &t.k_split : &t.k_tile;
+      (before_spatial ? t.splits : t.kt) *= q.ext;
+    } else {
+      before_spatial = false;
+      if (g == AG_M) { L = &t.m_grid; t.grid_m *= q.ext; }
+      else if (g == AG_N) { L = &t.n_grid; t.grid_n *= q.ext; }
+      else return false;
+    }
+    if (L->n >= 8) return false;
+    const int k = L->n++;
+    L->ext[k] = q.ext;
+    L->xn[k] = xd[0][v];
+    L->xh[k] = xd[1][v];
+    L->xw[k] = xd[2][v];
+    L->xc[k] = xd[3][v];
+    if (g == AG_K) {
+      if (cy[v] % ncols) return false;
+      L->kf[k] = cy[v] / ncols;  // weight row (flattened r, s, ci) of the K-major copy
+    } else if (g == AG_N) {
+      L->co[k] = cy[v];          // output-channel offset of an N tile
+    } else if (cy[v] != 0) {
+      return false;
+    }
+    L->cc[k] = cc[v];
+    if (cc[v] % 4) return false;  // float4 epilogue stores
+  }
+  if (t.c0 % 4 || t.cc_h1 % 4 || t.cc_w1 % 4) return false;
+  const int64_t stage = 128 * 64 * 2 + t.bn * 64 * 2;
+  const bool cluster = t.splits > 1;
+  const int64_t rows_per = (64 + t.splits - 1) / t.splits;
+  const int64_t red = cluster ? t.splits * rows_per * (t.bn + 4) * 4 : 64 * (t.bn + 4) * 4;
+  int64_t avail = lim.max_smem - 2048 - (cluster ? red : 0);
+  t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / stage));
+  t.stages = std::min<int64_t>(t.stages, 8);
+  t.smem_bytes = (cluster ? t.stages * stage + red : std::max(t.stages * stage, red)) + 1024 + 256;
+  return true;
+}
+
+}  // namespace
+
 GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const DeviceLimits& lim) {
   GeneralPlan plan;
   std::string err;
@@ -209,7 +339,7 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
       if (!affine_coeffs((*idx)[static_cast<size_t>(w.wit_dim[a])], nv, &coef[a], &c0) || c0 != 0)
         return unsupported("non-affine index (fused loop) in the contraction");
     }
-    struct LP { int axis; int64_t ext, stride; Kind kind; int var; };
+    using LP = LoopPart;
     std::vector<LP> lps;
     for (const Stmt* l : blk.loops) {
       int axis = -1;
@@ -343,6 +473,32 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
         if (!ok || ((cv != 0) != inb)) return unsupported("Select guard is not the load's in-bounds predicate");
       }
     }
+    // ---- TCGEN05 conv: innermost [p 8][q 8][co BN][ci 64] (bf16) ----
+    if (lim.bf16 && tc_conv_plan(w, p, s, xl, yl, lps, cond != nullptr, lim, &step.conv)) {
+      step.family = F_TCCONV;
+      step.x_buf = xl->buffer;
+      step.y_buf = yl->buffer;
+      step.c_buf = s->buffer;
+      plan.family = F_TCCONV;
+      const TcConvCfg& t = step.conv;
+      int32_t* o = plan.cfg;
+      o[0] = static_cast<int32_t>(t.grid_m); o[1] = static_cast<int32_t>(t.grid_n);
+      o[2] = static_cast<int32_t>(t.bn); o[3] = static_cast<int32_t>(t.splits);
+      o[4] = static_cast<int32_t>(t.kt); o[5] = static_cast<int32_t>(t.stages);
+      o[6] = static_cast<int32_t>(t.smem_bytes / 1024);
+      plan.steps.push_back(step);
+      if (t.bn > 256 || t.splits > 16) { plan.status = P_ILLEGAL; plan.why = "conv tile beyond tcgen05 limits"; return plan; }
+      if (t.smem_bytes > lim.max_smem) { plan.status = P_ILLEGAL; plan.why = "smem above limit"; return plan; }
+      if (s->epilogue) {
+        GStep e;
+        e.family = F_GENERIC;
+        e.block = static_cast<int>(bi);
+        e.epilogue_pass = true;
+        plan.steps.push_back(e);
+      }
+      continue;
+    }
+
     A.ng = static_cast<int>(gdims.size());
     for (int g = 0; g < A.ng; ++g) {
       A.g0[g] = gconst[static_cast<size_t>(g)];

@@ -62,6 +62,23 @@ struct AffineCfg {
   int64_t smem_bytes;
 };
 
+// TCGEN05 implicit-GEMM conv: one 8x8 output-pixel box (64 rows, the upper
+// half of a 128-row UMMA tile) x BN output channels x 64 input channels per
+// k-tile.  Per-part contributions to the TMA coordinates of the 4-D X-side
+// box (n, h, w, c), to the flattened K index of the K-major weight copy, and
+// to the output address.
+struct CList {
+  int n;
+  int64_t ext[8], xn[8], xh[8], xw[8], xc[8], kf[8], cc[8], co[8];
+};
+struct TcConvCfg {
+  CList m_grid, n_grid, k_split, k_tile;
+  int64_t x_n0, x_h0, x_w0, x_c0;  // constant coordinates (inlined pad: -pad)
+  int64_t c0;                      // output address constant
+  int64_t cc_h1, cc_w1;            // output address per box row / box column
+  int64_t bn, splits, kt, stages, smem_bytes, grid_m, grid_n;
+};
+
 // Buffer ids of the candidate program, resolved by name against the runner's
 // device buffers.
 struct GStep {
@@ -69,7 +86,8 @@ struct GStep {
   int block;                // index into the candidate's GenProgram blocks
   bool epilogue_pass = false;
   AffineCfg aff{};
-  int x_buf = -1, y_buf = -1, c_buf = -1;  // candidate buffer ids (SIMT-A)
+  TcConvCfg conv{};
+  int x_buf = -1, y_buf = -1, c_buf = -1;  // candidate buffer ids (SIMT-A, TC-conv)
 };
 
 struct GeneralPlan {

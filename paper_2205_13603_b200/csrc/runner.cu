@@ -35,6 +35,7 @@
 #include "kernels.cuh"
 #include "plan.hpp"
 #include "simta.cuh"
+#include "tc_conv.cuh"
 
 using namespace lsb;
 
@@ -65,6 +66,22 @@ bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, 
   cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// bf16 NHWC activation [n][h][w][c] as a 4-D TMA map with an {64, 8, 8, 1}
+// box (one 8 x 8 pixel box x 64 channels); out-of-bounds boxes read zeros.
+bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(shape[3]), static_cast<cuuint64_t>(shape[2]),
+                        static_cast<cuuint64_t>(shape[1]), static_cast<cuuint64_t>(shape[0])};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(shape[3] * 2), static_cast<cuuint64_t>(shape[2] * shape[3] * 2),
+                           static_cast<cuuint64_t>(shape[1] * shape[2] * shape[3] * 2)};
+  cuuint32_t box[4] = {64, 8, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -115,6 +132,10 @@ struct ls_runner {
     for (size_t i = 0; i < gbuf.size(); ++i)
       if (gbuf[i] != c) cudaFree(gbuf[i]);
     gbuf.clear();
+    cudaFree(wt);
+    wt = nullptr;
+    tmap_wt.clear();
+    tmap_x.clear();
     gbuf_dtype.clear();
     general = false;
     cudaFree(x); cudaFree(y); cudaFree(yk); cudaFree(c); cudaFree(ref);
@@ -170,6 +191,26 @@ struct ls_runner {
   std::vector<int> gbuf_dtype;  // 0 bf16, 1 f32
   int64_t* gcode = nullptr;     // concatenated bytecode of the current batch
   size_t gcode_cap = 0;
+  // tcgen05 conv: K-major weight copy [n_cols][k_rows] and tensor-map caches
+  void* wt = nullptr;
+  int64_t wt_rows = 0, wt_cols = 0;
+  std::map<int, CUtensorMap> tmap_wt;         // by BN
+  std::map<const void*, CUtensorMap> tmap_x;  // by activation buffer
+
+  const CUtensorMap* map_wt(int bn) {
+    auto it = tmap_wt.find(bn);
+    if (it != tmap_wt.end()) return &it->second;
+    CUtensorMap m;
+    if (!wt || !make_kmajor_map(&m, wt, 1, wt_cols, wt_rows, bn)) return nullptr;
+    return &(tmap_wt[bn] = m);
+  }
+  const CUtensorMap* map_x(const void* buf, const int64_t* shape) {
+    auto it = tmap_x.find(buf);
+    if (it != tmap_x.end()) return &it->second;
+    CUtensorMap m;
+    if (!make_nhwc_map(&m, const_cast<void*>(buf), shape)) return nullptr;
+    return &(tmap_x[buf] = m);
+  }
 
   bool general_buffers(const Plan& p, GenBuffers* B) {
     const GenProgram& g = p.gp->gen;
@@ -192,7 +233,13 @@ struct ls_runner {
     for (const GStep& stp : p.gp->steps) {
       GenBlock g = p.gp->gen.blocks[static_cast<size_t>(stp.block)];
       bool ok = true;
-      if (stp.family == F_SIMTA) {
+      if (stp.family == F_TCCONV) {
+        if (B.dtype[stp.x_buf] != 0 || p.gp->gen.ndim[stp.x_buf] != 4) return false;
+        const CUtensorMap* mx = map_x(B.ptr[stp.x_buf], B.shape[stp.x_buf]);
+        const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
+        if (!mx || !mw) return false;
+        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st);
+      } else if (stp.family == F_SIMTA) {
         ok = launch_simta(B.ptr[stp.x_buf], B.ptr[stp.y_buf], static_cast<float*>(B.ptr[stp.c_buf]), stp.aff, bf16, dl,
                           flag, st);
       } else if (stp.family == F_NESTGEN) {
@@ -378,8 +425,25 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
   LSB_CUDA(cudaStreamSynchronize(r->st));
   cudaFree(code);
   for (void* t : temps) cudaFree(t);
+  // K-major weight copy for the tcgen05 conv family: the contraction's
+  // weight viewed as [k_rows][n_cols] (n = its contiguous last dim)
   r->tc_ok = false;
   r->lim.bf16 = false;
+  for (size_t b = 0; b < nb && r->bf16; ++b) {
+    if (gw.buffers[b] != gw.y_buf || gw.roles[b] != 0) continue;
+    const std::vector<int64_t>& sh = gw.shapes[b];
+    int64_t elems = 1;
+    for (int64_t x : sh) elems *= x;
+    r->wt_cols = sh.back();
+    r->wt_rows = elems / r->wt_cols;
+    if (r->wt_rows % 64 || r->wt_cols % 16) break;
+    LSB_CUDA(cudaMalloc(&r->wt, static_cast<size_t>(elems) * 2));
+    launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
+                          r->wt_rows, r->wt_cols, r->st);
+    LSB_CUDA(cudaGetLastError());
+    LSB_CUDA(cudaStreamSynchronize(r->st));
+    r->lim.bf16 = true;
+  }
   r->have_workload = true;
   return LS_OK;
 }
@@ -413,6 +477,13 @@ ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* pro
   }
   DeviceLimits lim;
   lim.bf16 = !general && dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
+  if (general && dtype == LS_DTYPE_BF16)
+    for (size_t b = 0; b < gw.buffers.size(); ++b)
+      if (gw.buffers[b] == gw.y_buf && gw.roles[b] == 0) {
+        int64_t elems = 1;
+        for (int64_t x : gw.shapes[b]) elems *= x;
+        lim.bf16 = (elems / gw.shapes[b].back()) % 64 == 0 && gw.shapes[b].back() % 16 == 0;
+      }
   std::vector<Plan> plans;
   plan_all(w, general ? &gw : nullptr, lim, programs, lens, n, &plans);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
@@ -640,7 +711,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   {
     auto rank = [](int fam) {
       switch (fam) {
-        case F_TC: return 0;
+        case F_TC: case F_TCCONV: return 0;
         case F_SIMT: case F_SIMTA: return 1;
         case F_NAIVE: case F_GENERIC: return 2;
         default: return 3;  // LOOPNEST, NESTGEN

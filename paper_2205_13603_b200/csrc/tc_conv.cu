@@ -1,0 +1,268 @@
+// TCGEN05 implicit-GEMM convolution (NHWC): one CTA owns an 8 x 8 box of
+// output pixels x BN output channels.  Each k-tile is one (filter tap, 64
+// input channels) pair: TMA loads the 8 x 8 x 64 input box at the tap's shifted
+// coordinates straight from the (unpadded or padded) activation tensor into
+// the upper 64 rows of a 128-row, 128-byte-swizzled operand stage -- the
+// zero padding of the convolution is TMA's out-of-bounds fill, so an inlined
+// pad stage costs nothing -- and the matching [BN x 64] slice of the K-major
+// weight copy.  The lower 64 rows stay zero, so the UMMA tile is 128 x BN
+// with half its rows live (M = 64 output pixels per box).
+//
+// Warp roles and pipeline as in tc_gemm.cu (TMA producer lane, single MMA
+// issuer, S-stage mbarrier ring, PDL).  Filter-row parts hoisted above every
+// spatial loop are split-K: the split CTAs form a cluster and reduce through
+// DSMEM (each CTA owns a slice of the 64 live rows).  Coordinates of every
+// box come from per-part contributions computed by the planner
+// (affine.cpp tc_conv_plan), so any loop order of the scheduled nest maps to
+// the same kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+#include "tc_conv.cuh"
+
+namespace lsb {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kStageA = 128 * 64 * 2;  // A stage bytes (rows 64..127 zero)
+constexpr int kLiveA = 64 * 64 * 2;    // bytes TMA writes per A stage
+constexpr int kRows = 64;
+constexpr int kMaxClusterSplits = 16;
+
+struct TcConvArgs {
+  float* c;
+  TcConvCfg g;
+  int bn, splits, kt, stages, mode;
+  uint32_t idesc, tmem_cols;
+};
+
+struct Coord {
+  int64_t n, h, w, c, kf, co, cc;
+};
+
+__device__ __forceinline__ void add_parts(const CList& L, int64_t idx, Coord& a) {
+  for (int i = L.n - 1; i >= 0; --i) {
+    const int64_t v = idx % L.ext[i];
+    idx /= L.ext[i];
+    a.n += v * L.xn[i];
+    a.h += v * L.xh[i];
+    a.w += v * L.xw[i];
+    a.c += v * L.xc[i];
+    a.kf += v * L.kf[i];
+    a.co += v * L.co[i];
+    a.cc += v * L.cc[i];
+  }
+}
+
+__global__ void __launch_bounds__(128, 1)
+tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+               const __grid_constant__ TcConvArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const int b_bytes = a.bn * 64 * 2;
+  const uint32_t a0 = base;
+  const uint32_t b0 = base + a.stages * kStageA;
+  const int red_ld = a.bn + 4;
+  const uint32_t stage_end = b0 + a.stages * b_bytes;
+  const int S_cl = a.mode == 1 ? a.splits : 1;
+  const int rows_per = (kRows + S_cl - 1) / S_cl;
+  const uint32_t red = a.mode == 1 ? ((stage_end + 15u) & ~15u) : base;
+  const uint32_t red_bytes = a.mode == 1 ? static_cast<uint32_t>(S_cl * rows_per * red_ld * 4)
+                                         : static_cast<uint32_t>(kRows * red_ld * 4);
+  const uint32_t red_end = red + red_bytes;
+  const uint32_t bars = ((stage_end > red_end ? stage_end : red_end) + 15u) & ~15u;
+  const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // the dead lower half of every A stage: zero once, visible to the tensor core
+  for (int s = 0; s < a.stages; ++s) {
+    uint4* z = reinterpret_cast<uint4*>(gbase + s * kStageA + kLiveA);
+    for (int i = threadIdx.x; i < kLiveA / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(a.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmw)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // tile origin: output-pixel box (grid y), channel tile (grid x), split (grid z)
+  Coord o{a.g.x_n0, a.g.x_h0, a.g.x_w0, a.g.x_c0, 0, 0, a.g.c0};
+  add_parts(a.g.m_grid, blockIdx.y, o);
+  add_parts(a.g.n_grid, blockIdx.x, o);
+  add_parts(a.g.k_split, blockIdx.z, o);
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    const uint32_t stage_bytes = kLiveA + b_bytes;
+    for (int kt = 0; kt < a.kt; ++kt) {
+      const int s = kt % a.stages;
+      const uint32_t ph = (kt / a.stages) & 1;
+      if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
+      Coord t = o;
+      add_parts(a.g.k_tile, kt, t);
+      mbar_expect_tx(full + 8 * s, stage_bytes);
+      tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(t.c), static_cast<int>(t.w),
+                  static_cast<int>(t.h), static_cast<int>(t.n));
+      tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(t.kf), static_cast<int>(t.co), 0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread) ----
+    for (int kt = 0; kt < a.kt; ++kt) {
+      const int s = kt % a.stages;
+      const uint32_t ph = (kt / a.stages) & 1;
+      mbar_wait(full + 8 * s, ph);
+      tc_fence_after();
+      const uint32_t sa = a0 + s * kStageA, sb = b0 + s * b_bytes;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+      umma_commit(empty + 8 * s);
+    }
+    umma_commit(done);
+  }
+
+  // ---- epilogue: rows 0..63 (TMEM lanes of warps 0 and 1) ----
+  mbar_wait(done, 0);
+  __syncwarp();
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  const int c4 = a.bn / 4;
+  float* cbase = a.c + o.cc;
+  auto out_row = [&](int r) { return cbase + (r >> 3) * a.g.cc_h1 + (r & 7) * a.g.cc_w1; };
+  if (a.mode == 1) {
+    const uint32_t me = cluster_rank();
+    if (warp < 2) {
+      const int owner = row / rows_per, lr = row - owner * rows_per;
+      const uint32_t dst =
+          map_peer(red + static_cast<uint32_t>(((static_cast<int>(me) * rows_per + lr) * red_ld) * 4), owner);
+      for (int c0 = 0; c0 < a.bn; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_cluster_f4(dst + static_cast<uint32_t>((c0 + 4 * q) * 4), v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                        v[4 * q + 3]);
+      }
+    }
+    cluster_sync_all();
+    const int r_lo = static_cast<int>(me) * rows_per;
+    const int nrows = max(0, min(kRows, r_lo + rows_per) - r_lo);
+    const float* rb = reinterpret_cast<const float*>(gbase + (red - base));
+    for (int e = threadIdx.x; e < nrows * c4; e += 128) {
+      const int lr2 = e / c4, cc = (e % c4) * 4;
+      float4 acc = *reinterpret_cast<const float4*>(rb + lr2 * red_ld + cc);
+#pragma unroll
+      for (int q = 1; q < kMaxClusterSplits; ++q)
+        if (q < S_cl) {
+          const float4 v = *reinterpret_cast<const float4*>(rb + (q * rows_per + lr2) * red_ld + cc);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      *reinterpret_cast<float4*>(out_row(r_lo + lr2) + cc) = acc;
+    }
+  } else {
+    if (warp < 2) {
+      float* stg = reinterpret_cast<float*>(gbase) + row * red_ld;
+      for (int c0 = 0; c0 < a.bn; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stg + c0 + 4 * q) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    }
+    __syncthreads();
+    const float* sb = reinterpret_cast<const float*>(gbase);
+    for (int e = threadIdx.x; e < kRows * c4; e += 128) {
+      const int r = e / c4, cc = (e % c4) * 4;
+      *reinterpret_cast<float4*>(out_row(r) + cc) = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+  }
+}
+
+}  // namespace
+
+bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
+                    cudaStream_t st) {
+  static int max_dyn = -1;
+  if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
+  if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
+  if (g.splits > kMaxClusterSplits || g.grid_m > 65535 || g.grid_n > 65535) return false;
+  TcConvArgs a;
+  a.c = c;
+  a.g = g;
+  a.bn = static_cast<int>(g.bn);
+  a.splits = static_cast<int>(g.splits);
+  a.kt = static_cast<int>(g.kt);
+  a.stages = static_cast<int>(g.stages);
+  a.mode = g.splits == 1 ? 0 : 1;
+  a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(g.bn >> 3) << 17) |
+            (static_cast<uint32_t>(128 >> 4) << 24);
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(g.bn)) cols <<= 1;
+  a.tmem_cols = cols;
+  static bool nonportable = false;
+  if (a.mode == 1 && g.splits > 8 && !nonportable) {
+    if (cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    nonportable = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g.grid_n), static_cast<unsigned>(g.grid_m), static_cast<unsigned>(g.splits));
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = static_cast<size_t>(g.smem_bytes);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = a.mode == 1 ? static_cast<unsigned>(g.splits) : 1u;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
+  const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
+  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, a) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cudaGetLastError() == cudaSuccess;
+}
+
+}  // namespace lsb

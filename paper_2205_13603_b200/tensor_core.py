@@ -12,6 +12,11 @@ structurally: the three innermost loops
 outside every spatial loop becomes split-K, and the remaining spatial parts
 become the CTA grid.
 
+NHWC conv2d (implicit GEMM): output pixels are tiled into 8 x 8 boxes (the
+M rows of the tile), output channels into BN = 16 * t, input channels into
+64-wide k-tiles, and the filter rows r into (split-K ways, in-loop rows):
+``[r_split][n][p0][q0][co0][r_in][s][ci0][p 8][q 8][co BN][ci 64]``.
+
 Decisions (all traced, so search and mutation see them):
   * N: ``split(j, [m/16, 16])`` then ``sample_perfect_tile(j_hi, 2)`` gives
     ``BN = 16 * t`` (tcgen05 N granularity is 16 at M=128); BN > 256 is left to
@@ -63,6 +68,43 @@ def _contraction_roles(ir, stmt, loops):
     return roles
 
 
+PIX = 8      # output-pixel box edge: 8 x 8 pixels feed the upper 64 rows of a 128-row UMMA tile
+CI_TILE = 64  # input channels per k-tile (one 128-byte swizzle row of bf16)
+
+
+def _conv_roles(ir, stmt, loops):
+    """For O[n,p,q,co] += X[n, p+r(+c), q+s(+c), ci] * W[r,s,ci,co] (the NHWC
+    implicit GEMM of `workloads.conv2d_nhwc`): var names by role, or None."""
+    v = stmt.value
+    if not (isinstance(v, ir.BinOp) and v.op == "mul" and isinstance(v.b, ir.Load)):
+        return None
+    x, w = v.a, v.b
+    if isinstance(x, ir.Select) and isinstance(x.then, ir.Load) \
+            and isinstance(x.other, ir.IntConst) and x.other.value == 0:
+        x = x.then  # pad inlined as a guarded load (zero outside the image)
+    if not isinstance(x, ir.Load):
+        return None
+    if len(stmt.indices) != 4 or len(x.indices) != 4 or len(w.indices) != 4:
+        return None
+    if not all(isinstance(e, ir.Var) for e in tuple(stmt.indices) + tuple(w.indices)):
+        return None
+    n, p, q, co = (e.name for e in stmt.indices)
+    r, s, ci, co2 = (e.name for e in w.indices)
+    if co2 != co:
+        return None
+    if not (isinstance(x.indices[0], ir.Var) and x.indices[0].name == n
+            and isinstance(x.indices[3], ir.Var) and x.indices[3].name == ci):
+        return None
+    for d, (a, b) in ((1, (p, r)), (2, (q, s))):
+        dec = ir.affine_coeffs(x.indices[d])
+        if dec is None or dec[0] != {a: 1, b: 1}:
+            return None
+    names = [l.var for l in loops]
+    if sorted(names) != sorted([n, p, q, co, r, s, ci]):
+        return None
+    return {"n": n, "p": p, "q": q, "co": co, "r": r, "s": s, "ci": ci}
+
+
 def _module_class():
     ls = loopsched()
     ir = ls.ir
@@ -83,17 +125,36 @@ def _module_class():
             loops = [l for _, l in ir.enclosing_loops(state.program.root, path)]
             if any(l.kind != "serial" for l in loops):
                 return False
+            ext = {l.var: l.extent for l in loops}
+            conv = _conv_roles(ir, stmt, loops)
+            if conv is not None:
+                return (ext[conv["p"]] % PIX == 0 and ext[conv["q"]] % PIX == 0
+                        and ext[conv["ci"]] % CI_TILE == 0 and ext[conv["co"]] % N_GRAIN == 0)
             roles = _contraction_roles(ir, stmt, loops)
             if roles is None:
                 return False
-            ext = {l.var: l.extent for l in loops}
             return (ext[roles["m"][0]] % UMMA_M == 0
                     and ext[roles["n"][0]] % N_GRAIN == 0
                     and ext[roles["k"][0]] % BLOCK_K == 0)
 
+        def _apply_conv(self, state, block, loops, c):
+            refs = state.get_loops(block)
+            by_var = {state._resolve_loop(r)[1].var: r for r in refs}
+            ext = {l.var: l.extent for l in loops}
+            p0, p1 = state.split(by_var[c["p"]], [ext[c["p"]] // PIX, PIX])
+            q0, q1 = state.split(by_var[c["q"]], [ext[c["q"]] // PIX, PIX])
+            co_hi, co16 = state.split(by_var[c["co"]], [ext[c["co"]] // N_GRAIN, N_GRAIN])
+            co0, co1 = state.split(co_hi, state.sample_perfect_tile(co_hi, 2))
+            ci0, ci1 = state.split(by_var[c["ci"]], [ext[c["ci"]] // CI_TILE, CI_TILE])
+            rs, rt = state.split(by_var[c["r"]], state.sample_perfect_tile(by_var[c["r"]], 2))
+            state.reorder([rs, by_var[c["n"]], p0, q0, co0, rt, by_var[c["s"]], ci0, p1, q1, co1, co16, ci1])
+
         def apply(self, state, block):
             path, stmt = _block_stmt(state, block)
             loops = [l for _, l in ir.enclosing_loops(state.program.root, path)]
+            conv = _conv_roles(ir, stmt, loops)
+            if conv is not None:
+                return self._apply_conv(state, block, loops, conv)
             roles = _contraction_roles(ir, stmt, loops)
             refs = state.get_loops(block)
             by_var = {state._resolve_loop(r)[1].var: r for r in refs}

@@ -176,7 +176,7 @@ POPULATIONS = {
     "bert_ffn": (lambda: ls.gmm(128, 768, 3072), T.b200_space_config(), 8192),
     "bmm_qk": (lambda: W.batch_matmul(12, 128, 128, 64), T.b200_space_config(), 1024),
     "gmm512": (lambda: ls.gmm(512, 512, 512), ls.default_space_config(), 1024),
-    "conv2d": (lambda: W.conv2d_nhwc(), ls.default_space_config(), 512),
+    "conv2d": (lambda: W.conv2d_nhwc(), T.b200_space_config(), 512),
 }
 
 

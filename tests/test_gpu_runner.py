@@ -169,7 +169,9 @@ def test_measure_signature_matches_reference_runner():
 def test_conv2d_general_path_bit_exact(dtype):
     """conv2d NHWC (pad stage + implicit GEMM): the fp64 reference run equals
     the numpy oracle; SIMT-A (pad stage separate and pad inlined as a guarded
-    load), nest-generic and the unscheduled e0 match it bit-exactly."""
+    load), nest-generic, every tcgen05 conv candidate (TMA zero fill for the
+    inlined pad, cluster split-K over filter rows) and the unscheduled e0
+    match it bit-exactly."""
     import json
     hdr, pop = load_population("conv2d")
     e0 = hdr["e0"]
@@ -182,6 +184,8 @@ def test_conv2d_general_path_bit_exact(dtype):
     inlined = [i for i, p in enumerate(progs)
                if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
     picks = pick(plans, "simt_affine", 6) + inlined[:4] + pick(plans, "nestgen", 1)
+    if dtype == "bf16":
+        picks += [i for i, x in enumerate(plans) if x["family"] == "tcgen05_conv"]
     assert picks
     for i in picks:
         res, = r.measure_programs([progs[i]])

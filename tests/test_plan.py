@@ -80,7 +80,11 @@ def test_conv2d_general_families():
     res = plan(hdr["e0"], [p["program"] for p in pop])
     fams = Counter((r["family"], r["status"]) for r in res)
     assert fams[("simt_affine", "OK")] > 100 and fams[("nestgen", "OK")] > 0
+    assert fams[("tcgen05_conv", "OK")] > 10
     for r in res:
+        if r["family"] == "tcgen05_conv":
+            gm, gn, bn, splits, kt = r["cfg"][:5]
+            assert gm * 64 == 56 * 56 and gn * bn == 64 and splits * kt * 64 == 3 * 3 * 64
         if r["family"] == "simt_affine":
             gb, gm, gn, tb, tm, tn, rb, rm, rn, bk, kt = r["cfg"][:11]
             assert gm * tm * rm == 56 * 56 and gn * tn * rn == 64 and bk * kt == 3 * 3 * 64
