@@ -237,18 +237,16 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
         if (before_spatial) t.splits *= merged[i].extent;
         else t.kt *= merged[i].extent;
       }
-      // split-K above 16 ways cannot form one cluster: fp32 atomics into a zeroed C
-      plan.needs_zero = t.splits > 16;
-      int64_t stage = 128 * 64 * 2 + t.bn * 64 * 2;
-      // epilogue buffer: cluster split-K receives splits x ceil(128/splits)
-      // padded rows in its own region; otherwise the tile reuses the ring
-      bool cluster = t.splits > 1 && t.splits <= 16;
-      int64_t rows_per = (128 + t.splits - 1) / t.splits;
-      int64_t red = cluster ? t.splits * rows_per * (t.bn + 4) * 4 : 128 * (t.bn + 4) * 4;
-      int64_t avail = lim.max_smem - 2048 - (cluster ? red : 0);
-      t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / stage));
+      // stage count: as many k-tiles as fit beside the reduction buffer (<= 8)
+      const int64_t tiles = t.batch * t.grid_m * t.grid_n;
+      TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles, t.grid_n, lim.max_smem);
+      int64_t avail = lim.max_smem - 1024 - 256 - g0.recv;
+      t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / g0.stage_bytes));
       t.stages = std::min<int64_t>(t.stages, 8);
-      t.smem_bytes = (cluster ? t.stages * stage + red : std::max(t.stages * stage, red)) + 1024 + 256;
+      TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles, t.grid_n, lim.max_smem);
+      plan.needs_zero = g.mode == 3;
+      t.direct = g.direct;
+      t.smem_bytes = g.smem;
       int32_t* c = plan.cfg;
       c[0] = static_cast<int32_t>(t.batch); c[1] = static_cast<int32_t>(t.grid_m);
       c[2] = static_cast<int32_t>(t.grid_n); c[3] = static_cast<int32_t>(t.bn);

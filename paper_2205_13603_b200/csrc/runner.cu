@@ -114,6 +114,7 @@ struct ls_runner {
   double* ref = nullptr;
   Strides s{};
   CUtensorMap tmap_a{};
+  std::map<int, CUtensorMap> tmap_am;  // A maps by box rows (TMA multicast slices)
   std::map<int, CUtensorMap> tmap_b;
   unsigned long long* deadline = nullptr;  // device deadline state: [0] deadline, [1] arm time, [2] best ns
   int* flags = nullptr;                    // per-candidate timeout flags
@@ -141,14 +142,17 @@ struct ls_runner {
     cudaFree(x); cudaFree(y); cudaFree(yk); cudaFree(c); cudaFree(ref);
     x = y = yk = nullptr; c = nullptr; ref = nullptr;
     tmap_b.clear();
+    tmap_am.clear();
     have_workload = false;
   }
   void release() {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
     release_workload();
-    cudaFree(deadline); cudaFree(flags); cudaFree(parity); cudaFree(gcode);
+    cudaFree(deadline); cudaFree(flags); cudaFree(parity); cudaFree(gcode); cudaFree(tcsync);
     gcode = nullptr;
+    tcsync = nullptr;
+    tcsync_cap = 0;
     deadline = nullptr; flags = nullptr; parity = nullptr;
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
@@ -174,6 +178,14 @@ struct ls_runner {
     return LS_OK;
   }
 
+  const CUtensorMap* map_a(int rows) {
+    if (rows == 128) return &tmap_a;
+    auto it = tmap_am.find(rows);
+    if (it != tmap_am.end()) return &it->second;
+    CUtensorMap m;
+    if (!make_kmajor_map(&m, x, w.extent[R_BATCH], w.extent[R_M], w.extent[R_K], rows)) return nullptr;
+    return &(tmap_am[rows] = m);
+  }
   const CUtensorMap* map_b(int bn) {
     auto it = tmap_b.find(bn);
     if (it != tmap_b.end()) return &it->second;
@@ -184,6 +196,33 @@ struct ls_runner {
 
   // one launch of a planned candidate (plus its zeroing memset)
   unsigned long long* trace = nullptr;  // set only by ls_runner_trace_tc
+  // split-K ticket slots (tc_geom mode 2): 2 x kTcSyncSlots words per such
+  // candidate of the current call, zeroed before its first launch
+  uint32_t* tcsync = nullptr;
+  size_t tcsync_cap = 0;  // words
+  std::vector<int64_t> sync_off;  // per candidate slot: word offset or -1
+
+  ls_status prepare_sync(const std::vector<Plan>& plans) {
+    sync_off.assign(plans.size(), -1);
+    size_t words = 0;
+    for (size_t i = 0; i < plans.size(); ++i) {
+      const Plan& p = plans[i];
+      if (p.status != P_OK || p.family != F_TC || p.gp) continue;
+      if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n, p.tc.grid_n).mode != 2)
+        continue;
+      sync_off[i] = static_cast<int64_t>(words);
+      words += 2 * kTcSyncSlots;
+    }
+    if (!words) return LS_OK;
+    if (words > tcsync_cap) {
+      cudaFree(tcsync);
+      tcsync = nullptr;
+      tcsync_cap = std::max(words, 2 * tcsync_cap);
+      LSB_CUDA(cudaMalloc(&tcsync, tcsync_cap * 4));
+    }
+    LSB_CUDA(cudaMemsetAsync(tcsync, 0, words * 4, st));
+    return LS_OK;
+  }
   // general workloads (multi-block / affine contraction)
   bool general = false;
   GeneralWorkload gw;
@@ -284,7 +323,11 @@ struct ls_runner {
         const CUtensorMap* mb = map_b(static_cast<int>(p.tc.bn));
         if (!mb) return false;
         TcLaunch L;
-        L.tmap_a = &tmap_a;
+        const TcGeom g = tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n,
+                                 p.tc.grid_n);
+        const CUtensorMap* ma = map_a(128 / g.mc);
+        if (!ma) return false;
+        L.tmap_a = ma;
         L.tmap_b = mb;
         L.c = c;
         L.sc_b = w.sc[R_BATCH];
@@ -300,7 +343,11 @@ struct ls_runner {
         L.grid_m = static_cast<int>(p.tc.grid_m);
         L.grid_n = static_cast<int>(p.tc.grid_n);
         L.smem_bytes = static_cast<int>(p.tc.smem_bytes);
+        L.direct = p.tc.direct;
         L.trace = trace;
+        L.sync = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
+                     ? tcsync + sync_off[static_cast<size_t>(slot)]
+                     : nullptr;
         return launch_tc_gemm(L, st);
       }
       default:
@@ -686,6 +733,8 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   const unsigned long long timeout_ns = static_cast<unsigned long long>(r->opts.timeout_ms * 1e6);
   LSB_CUDA(cudaMemsetAsync(r->flags, 0, static_cast<size_t>(n) * sizeof(int), r->st));
   LSB_CUDA(cudaMemsetAsync(r->parity, 0, static_cast<size_t>(n) * 16, r->st));
+  s = r->prepare_sync(plans);
+  if (s != LS_OK) return s;
   cudaEvent_t* E = r->ev.data();
   cudaEvent_t batch0;
   LSB_CUDA(cudaEventCreate(&batch0));
@@ -939,6 +988,12 @@ ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int 
   unsigned long long* d = nullptr;
   LSB_CUDA(cudaMalloc(&d, static_cast<size_t>(ctas) * 8 * 8 * launches));
   LSB_CUDA(cudaMemsetAsync(d, 0, static_cast<size_t>(ctas) * 8 * 8 * launches, r->st));
+  std::vector<Plan> one(1, plan);
+  ls_status ps = r->prepare_sync(one);
+  if (ps != LS_OK) {
+    cudaFree(d);
+    return ps;
+  }
   bool ok = true;
   for (int i = 0; i < launches && ok; ++i) {
     r->trace = d + static_cast<size_t>(i) * ctas * 8;

@@ -29,8 +29,10 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8)[: n.value * launches].ast
 t0 = a[:, 0].min()
 for L in range(launches):
     s = a[L * n.value:(L + 1) * n.value]
-    rel = (s[:, :6] - t0) / 1000.0
-    print(f"launch {L}: start [{rel[:,0].min():.2f},{rel[:,0].max():.2f}] setup+{np.median(rel[:,1]-rel[:,0]):.2f} "
-          f"firstload+{np.median(rel[:,2]-rel[:,1]):.2f} mma_done+{np.median(rel[:,3]-rel[:,2]):.2f} "
-          f"staged+{np.median(rel[:,4]-rel[:,3]):.2f} stored+{np.median(rel[:,5]-rel[:,4]):.2f} "
-          f"end [{rel[:,5].min():.2f},{rel[:,5].max():.2f}] us")
+    rel = (s[:, :7] - t0) / 1000.0
+    med = lambda j, i: float(np.median(rel[:, j] - rel[:, i]))
+    recv = med(5, 4) if (s[:, 5] > 0).all() else float("nan")
+    print(f"launch {L}: start [{rel[:,0].min():.2f},{rel[:,0].max():.2f}] setup+{med(1,0):.2f} "
+          f"firstload+{med(2,1):.2f} mma_done+{med(3,2):.2f} staged+{med(4,3):.2f} "
+          f"received+{recv:.2f} stored+{med(6,5) if recv == recv else med(6,4):.2f} "
+          f"end [{rel[:,6].min():.2f},{rel[:,6].max():.2f}] us")
