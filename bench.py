@@ -121,6 +121,17 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def profiled_traffic(workload):
+    """DRAM bytes per launch of the best kernel from the committed ncu --set
+    full capture (profiles/traffic.json, written by scripts/ncu_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            d = json.load(fh)[workload]
+        return {"dram_bytes_per_launch": d["dram_bytes"], "source": d["source"], "kernel": d["kernel"]}
+    except Exception:
+        return None
+
+
 def cpu_baseline(programs, model, budget_s=8.0):
     """The oracle port of the reference's Runner + predict on this host."""
     from oracle import oracle as O
@@ -247,15 +258,49 @@ def run_b200(args):
     dev_s = dev_ms / 1e3
     total_cands = len(texts) * world * args.steps
 
-    # best schedule of this rank (rank 0 reports its own; all ranks see the same kinds)
+    # best schedule of this rank (rank 0 reports its own; all ranks see the same kinds).
+    # Like a tuner's final measurement of its best records, the fastest few
+    # distinct schedules of the step are re-measured with long graph repeats
+    # (>= 0.5 ms per candidate), so the per-launch time carries no graph-launch
+    # overhead amortised over only 3 repeats; outside the timed region.
     ok = [r for r in results[-1] if r["status"] == "OK"]
     best = min(ok, key=lambda r: r["latency_ns"]) if ok else None
+    best_in_step_us = best["latency_ns"] / 1e3 if best else None
+    if ok:
+        order = sorted(range(len(texts)), key=lambda i: results[-1][i]["latency_ns"]
+                       if results[-1][i]["status"] == "OK" else float("inf"))
+        top, seen = [], set()
+        for i in order:
+            r = results[-1][i]
+            key = (r["family"], tuple(r["cfg"]))
+            if r["status"] != "OK" or key in seen:
+                continue
+            seen.add(key)
+            top.append(i)
+            if len(top) == args.final_top:
+                break
+        fin = B200Runner(device=local, dtype=dtype, min_repeats=50, max_repeats=2000, target_ms=0.5,
+                         timeout_ms=timeout_ms)
+        fin.set_workload(e0, inputs)
+        rem = fin.measure_programs([texts[i] for i in top])
+        fin.close()
+        rem_ok = [r for r in rem if r["status"] == "OK"]
+        if rem_ok:
+            best = min(rem_ok, key=lambda r: r["latency_ns"])
     peak_bf16, peak_hbm, peak_src = peaks()
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
     peak = peak_bf16 if dtype == "bf16" else fp32_peak
     best_tflops = flops / (best["latency_ns"] * 1e-9) / 1e12 if best else None
     from collections import Counter
     fam = Counter((r["family"], r["status"]) for r in results[-1])
+    # device time per outcome (estimate: checked launch + timed repeats of OK
+    # candidates, the abort time of timed-out ones)
+    fam_ms = Counter()
+    for r in results[-1]:
+        if r["status"] == "OK":
+            fam_ms[(r["family"], r["status"])] += r["latency_ns"] * (1 + r["repeats"]) / 1e6
+        elif r["status"] in ("TIMEOUT", "PARITY"):
+            fam_ms[(r["family"], r["status"])] += r["latency_ns"] / 1e6
     h2d = sum(len(t) for t in texts) * 2 + sum(v.nbytes for v in inputs.values())
     d2h = len(texts) * (104 + 100)
 
@@ -280,12 +325,17 @@ def run_b200(args):
                 "tflops": best_tflops, "frac_of_peak": best_tflops / peak,
                 "peak": peak, "peak_source": peak_src if dtype == "bf16" else "fp32 SIMT nominal",
                 "latency_us": best["latency_ns"] / 1e3, "family": best["family"], "cfg": best["cfg"],
+                "repeats": best["repeats"], "latency_us_in_step": best_in_step_us,
+                "measurement": f"top {args.final_top} distinct schedules of the last step re-measured, "
+                               "CUDA graph of >= 50 back-to-back launches (>= 0.5 ms) between CUDA events",
                 "speedup_vs_e0": base["latency_ns"] / best["latency_ns"]},
             "e0_baseline_us": base["latency_ns"] / 1e3,
             "outcomes": {f"{a}/{b}": c for (a, b), c in sorted(fam.items())},
+            "outcome_device_ms": {f"{a}/{b}": round(v, 3) for (a, b), v in sorted(fam_ms.items())},
             "roofline": None if best is None else {
                 "bound": "tensor" if dtype == "bf16" else "fp32-simt", "achieved": best_tflops,
-                "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak, "traffic": None,
+                "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
+                "traffic": profiled_traffic(args.workload),
                 "kernel": f"best candidate ({best['family']}), L2-warm back-to-back repeats"},
             "cpu_baseline": cpu,
         }
@@ -305,6 +355,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
+    ap.add_argument("--final-top", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--timeout-factor", type=float, default=10.0,
                     help="checked launches get clamp(factor x best-so-far, 0.05 ms, 2 x e0) before abort")
