@@ -52,6 +52,7 @@ int opt_in_dynamic_smem(const void* fn);
 struct TcLaunch {
   const void* tmap_a;  // CUtensorMap* (host memory, passed by value to the kernel)
   const void* tmap_b;
+  const void* tmap_c = nullptr;  // fp32 C [batch][M][N], box {32, 128, 1}, 128B swizzle (TMA epilogue)
   float* c;
   int64_t sc_b, sc_m;  // output strides (elements) for batch and M (N contiguous)
   int m, n, k;

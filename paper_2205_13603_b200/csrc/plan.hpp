@@ -79,11 +79,12 @@ struct TcCfg {
 //   mode 1: cluster       the splits CTAs of a tile form one cluster (<= 16)
 //                         and reduce-scatter their fp32 partials through
 //                         distributed shared memory (bulk DSMEM copies)
-//   mode 2: L2 reduction  split 0 zeroes the tile right after launch (its
-//                         loads are in flight), every split red.adds its
-//                         partial once the zeroing is released; an arrival
-//                         ticket per tile gives each launch its own epoch, so
-//                         there is no memset node between launches
+//   mode 2: L2 reduction  the first CTA of the tile to start zeroes it (its
+//                         loads are in flight), every split adds its partial
+//                         (TMA add-reduce) once the zeroing is released; the
+//                         arrival ticket per tile also gives each launch its
+//                         own epoch, so there is no memset node between
+//                         launches
 //   mode 3: mode 2 without ticket slots: fp32 atomics into a memset C
 // DSMEM moves ~20 B/clk per SM (B300_MICROARCH.md), below the SM's L2 red
 // bandwidth, so mode 2 is the default; mode 1 stays for experiments.

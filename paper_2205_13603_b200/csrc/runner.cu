@@ -70,6 +70,20 @@ bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 output [batch][M][N] as a 3-D TMA map with a {32, 128, 1} box and the
+// 128-byte swizzle (the tcgen05 epilogue's staged chunk layout).
+bool make_c_map(CUtensorMap* map, void* base, int64_t batch, int64_t m, int64_t n) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || n % 4 != 0) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(n * 4), static_cast<cuuint64_t>(m * n * 4)};
+  cuuint32_t box[3] = {32, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // bf16 NHWC activation [n][h][w][c] as a 4-D TMA map with an {64, 8, 8, 1}
 // box (one 8 x 8 pixel box x 64 channels); out-of-bounds boxes read zeros.
 bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape) {
@@ -114,6 +128,8 @@ struct ls_runner {
   double* ref = nullptr;
   Strides s{};
   CUtensorMap tmap_a{};
+  CUtensorMap tmap_c{};
+  bool have_tmap_c = false;
   std::map<int, CUtensorMap> tmap_am;  // A maps by box rows (TMA multicast slices)
   std::map<int, CUtensorMap> tmap_b;
   unsigned long long* deadline = nullptr;  // device deadline state: [0] deadline, [1] arm time, [2] best ns
@@ -143,6 +159,7 @@ struct ls_runner {
     x = y = yk = nullptr; c = nullptr; ref = nullptr;
     tmap_b.clear();
     tmap_am.clear();
+    have_tmap_c = false;
     have_workload = false;
   }
   void release() {
@@ -329,6 +346,7 @@ struct ls_runner {
         if (!ma) return false;
         L.tmap_a = ma;
         L.tmap_b = mb;
+        L.tmap_c = have_tmap_c ? &tmap_c : nullptr;
         L.c = c;
         L.sc_b = w.sc[R_BATCH];
         L.sc_m = w.sc[R_M];
@@ -676,6 +694,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
       set_error("cuTensorMapEncodeTiled failed for the A operand");
       return LS_ERR_CUDA;
     }
+    r->have_tmap_c = make_c_map(&r->tmap_c, r->c, B, M, N);
   }
   r->lim.bf16 = r->tc_ok;
   LSB_CUDA(cudaStreamSynchronize(r->st));

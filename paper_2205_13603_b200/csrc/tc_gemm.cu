@@ -47,6 +47,8 @@ struct TcArgs {
   int mc;                     // cluster of N-tiles sharing A by TMA multicast (cluster dims mc x 1 x cl)
   int debug;                  // experiment knob LSB_TC_DEBUG: 1 skip loads+MMA, 2 skip the epilogue,
                               // 4 skip the C stores, 8 skip the cluster exchange
+  int tma_epi;                // modes 0/2, BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
+  int early_poll;             // mode 2: observe the zeroing flag during the main loop (LSB_TC_EARLYPOLL)
   int direct;                 // push rows from registers (st.shared::cluster) instead of staged bulk copies
   uint32_t ring_or_tile;      // bytes from the aligned base to the receive buffer
   uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets, then [kTcSyncSlots] ready flags
@@ -58,9 +60,10 @@ struct TcArgs {
 constexpr int kTile = 128 * 64 * 2;  // A stage bytes
 
 __global__ void __launch_bounds__(128, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, TcArgs a) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+               const __grid_constant__ CUtensorMap tmc, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint32_t s_epoch;
+  __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -126,15 +129,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   float* ctile = a.c + batch * a.sc_b + static_cast<int64_t>(m_blk) * 128 * a.sc_m + static_cast<int64_t>(n_blk) * a.bn;
   const int c4 = a.bn / 4;
   if (a.mode == 2 && warp >= 2) {
-    // ---- mode 2: every split takes its arrival ticket now (off the critical
-    // path); split 0 zeroes the tile while its operands stream in ----
+    // ---- mode 2: every CTA takes its arrival ticket now (off the critical
+    // path); the first CTA of the tile to start zeroes it while its operands
+    // stream in, the others observe the zeroing before their epilogue ----
     const int t2 = threadIdx.x - 64;
-    uint32_t L = 0;
-    if (t2 == 0) {
-      L = atomicAdd(a.sync + tile, 1u) / static_cast<uint32_t>(a.parts);
-      s_epoch = L;
-    }
-    if (split == 0) {
+    if (t2 == 0) s_ticket = atomicAdd(a.sync + tile, 1u);
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const uint32_t t = s_ticket;
+    const uint32_t L = t / static_cast<uint32_t>(a.parts);
+    if (t % static_cast<uint32_t>(a.parts) == 0) {
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int e = t2; e < 128 * c4; e += 64) {
         const int r = e / c4, cc = (e % c4) * 4;
@@ -142,6 +145,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
       }
       asm volatile("bar.sync 1, 64;" ::: "memory");
       if (t2 == 0) st_release_u32(a.sync + kTcSyncSlots + tile, L + 1);  // cumulative over the barrier
+    } else if (t2 == 0 && a.early_poll) {
+      // first poll once the last k-tile has landed; back off between polls
+      const int last = a.kt - 1;
+      if (!(a.debug & 1)) mbar_wait(full + 8 * (last % a.stages), (last / a.stages) & 1);
+      while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < L + 1) __nanosleep(64);
     }
   }
 
@@ -218,6 +226,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
     }
     cluster_arrive();
     cluster_wait();  // every pushed row has landed
+  } else if (a.tma_epi) {
+    // TMEM -> 32-column chunks [128][32] fp32 with the 128-byte swizzle the C
+    // tensor map expects (16-byte unit q of row r at q ^ (r & 7): conflict-free)
+    for (int c0 = 0; c0 < a.bn; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld16_nowait(trow + c0, v);
+      tmem_ld16_nowait(trow + c0 + 16, v + 16);
+      tmem_wait();
+      uint8_t* chunk = gbase + (c0 / 32) * 16384 + row * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(chunk + ((q ^ (row & 7)) << 4)) =
+            make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                        __uint_as_float(v[4 * q + 3]));
+    }
+    fence_proxy_async_smem();  // read by the TMA engine
+    __syncthreads();
   } else {
     // TMEM -> padded smem tile over the finished ring
     float* stg = reinterpret_cast<float*>(gbase) + row * a.ld;
@@ -250,16 +275,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
 
   const float* stile = reinterpret_cast<const float*>(gbase);
   if (a.mode != 1) {
-    if (a.mode == 2 && split != 0) {
-      // wait for this launch's zeroing of the tile (long done in practice)
-      if (threadIdx.x == 0) {
-        const uint32_t L = s_epoch;  // written by thread 64 before the staging barrier
-        while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < L + 1) {
+    if (a.mode == 2 && !a.early_poll && s_ticket % static_cast<uint32_t>(a.parts) != 0) {
+      if (threadIdx.x == 0)
+        while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.parts) + 1) {
         }
-      }
       __syncthreads();
     }
     if (tr && threadIdx.x == 0) tr[5] = gtime();
+    if (a.tma_epi) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async_global();  // the (acquired) zeroing precedes the async-proxy reduction
+        for (int c0 = 0; c0 < a.bn; c0 += 32) {
+          const uint32_t src = base + (c0 / 32) * 16384;
+          if (a.mode == 0) tma_store_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
+          else tma_reduce_add_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
+        }
+        bulk_commit();
+        bulk_wait_all();  // complete before exit: the next launch's zeroing follows grid completion
+      }
+    } else
     for (int e = threadIdx.x; e < 128 * c4; e += 128) {
       const int r = e / c4, cc = (e % c4) * 4;
       const float4 acc = *reinterpret_cast<const float4*>(stile + r * a.ld + cc);
@@ -349,6 +383,10 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.debug = debug;
 
   a.direct = L.direct ? 1 : 0;
+  static const int early_poll = getenv("LSB_TC_EARLYPOLL") ? atoi(getenv("LSB_TC_EARLYPOLL")) : 0;
+  a.early_poll = early_poll;
+  static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
+  a.tma_epi = L.tmap_c && !no_tma_epi && (g.mode == 0 || g.mode == 2) && L.bn % 32 == 0 ? 1 : 0;
   a.ring_or_tile = static_cast<uint32_t>(((L.direct ? g.ring : std::max(g.ring, g.tile)) + 15) & ~15LL);
   a.sync = L.sync;
   a.trace = L.trace;
@@ -384,7 +422,8 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   cfg.numAttrs = 2;
   const CUtensorMap ta = *static_cast<const CUtensorMap*>(L.tmap_a);
   const CUtensorMap tb = *static_cast<const CUtensorMap*>(L.tmap_b);
-  if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ta, tb, a) != cudaSuccess) {
+  const CUtensorMap tc = L.tmap_c ? *static_cast<const CUtensorMap*>(L.tmap_c) : tb;
+  if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ta, tb, tc, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }

@@ -74,6 +74,30 @@ def test_all_tcgen05_candidates_exact_bert_ffn():
     r.close()
 
 
+@pytest.mark.parametrize("name", ["bert_ffn", "bmm_qk"])
+def test_tcgen05_back_to_back_repeats_exact(name):
+    # C after a CUDA graph of >= 8 back-to-back launches (PDL chain, split-K
+    # arrival tickets and in-kernel zeroing across launches) of every distinct
+    # tcgen05 configuration equals the oracle bit for bit
+    hdr, pop = load_population(name)
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    r = make_runner("bf16", min_repeats=8, max_repeats=8)
+    r.set_workload(e0, seed=2)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 2)).values()))
+    plans = r.plan_programs(progs)
+    seen = {}
+    for i, p in enumerate(plans):
+        if p["family"] == "tcgen05" and p["status"] == "OK":
+            seen.setdefault(tuple(p["cfg"]), i)
+    assert seen
+    for cfg, i in seen.items():
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] == "OK" and res["mismatches"] == 0 and res["repeats"] == 8, (cfg, res)
+        assert np.array_equal(r.last_output().astype(np.float64), want), cfg
+    r.close()
+
+
 def test_float_inputs_tolerance():
     # N(0,1) inputs: fp32 candidates within rtol 1e-4 of fp64 math; bf16 inputs
     # are rounded once at upload, the candidates then accumulate in fp32.
