@@ -221,12 +221,19 @@ def run_b200(args):
     devbatch = DeviceBatch(texts, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
+    host_split = []
+
     def step():
         t0 = time.perf_counter()
         runner.set_workload(e0, inputs)
+        t1 = time.perf_counter()
         res = runner.measure_programs(texts)
+        t2 = time.perf_counter()
         lats, feats, pred = scorer.analyze(texts, model=model)
         wall = time.perf_counter() - t0
+        st = runner.debug_stats()
+        host_split.append([round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
+                           round(1e3 * (time.perf_counter() - t2), 1), round(st["phase_a_host_ms"], 1), round(st["phase_b_host_ms"], 1)])
         devbatch.analyze(model=model)
         dev_ms = runner.elapsed_ms() + devbatch.elapsed_ms()
         return res, wall, dev_ms, runner.launch_count() + 2
@@ -318,7 +325,10 @@ def run_b200(args):
                                   "timeout_cap_ms": round(timeout_ms, 4), "timeout_factor": args.timeout_factor,
                                   "timeout_floor_ms": 0.05, "parity": "exact (integer inputs)"}},
             "e2e": {"value": total_cands / wall_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "step_ms": [round(1e3 * w, 2) for w in walls]},
+            "device_step_ms": [round(d, 2) for d in devs],
+            "host_split_ms": {"cols": ["set_workload", "measure", "analyze", "phaseA_host", "phaseB_host"],
+                              "steps": host_split[-args.steps:]},
             "gpu_launches": launches,
             "clocks": clk,
             "best_schedule": None if best is None else {

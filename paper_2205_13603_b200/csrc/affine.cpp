@@ -273,6 +273,129 @@ bool tc_conv_plan(const GeneralWorkload& w, const Program& p, const Stmt* s, con
 
 }  // namespace
 
+// Quasi-affine decomposition of an index expression over the loops of one
+// block: sum of coef * ((v_l / div) % mod) terms + constant (generic.hpp).
+bool qdecomp(const Expr* e, const std::vector<int>& loop_of_var, int64_t scale, QSum* q);
+
+bool qsingle(const Expr* e, const std::vector<int>& loop_of_var, QTerm* t) {
+  QSum tmp;
+  if (!qdecomp(e, loop_of_var, 1, &tmp) || tmp.n != 1 || tmp.c0 != 0 || tmp.t[0].coef != 1) return false;
+  *t = tmp.t[0];
+  return true;
+}
+
+bool qdecomp(const Expr* e, const std::vector<int>& loop_of_var, int64_t scale, QSum* q) {
+  switch (e->op) {
+    case Op::Int: q->c0 += scale * e->value; return true;
+    case Op::Var: {
+      if (e->var < 0 || static_cast<size_t>(e->var) >= loop_of_var.size() || loop_of_var[e->var] < 0) return false;
+      if (q->n == kQMax) return false;
+      q->t[q->n++] = QTerm{loop_of_var[e->var], 1, 0, 0, scale};
+      return true;
+    }
+    case Op::Add: return qdecomp(e->kids[0], loop_of_var, scale, q) && qdecomp(e->kids[1], loop_of_var, scale, q);
+    case Op::Sub: return qdecomp(e->kids[0], loop_of_var, scale, q) && qdecomp(e->kids[1], loop_of_var, -scale, q);
+    case Op::Mul:
+      if (e->kids[0]->op == Op::Int) return qdecomp(e->kids[1], loop_of_var, scale * e->kids[0]->value, q);
+      if (e->kids[1]->op == Op::Int) return qdecomp(e->kids[0], loop_of_var, scale * e->kids[1]->value, q);
+      return false;
+    case Op::FloorDiv:
+    case Op::Mod: {
+      if (e->kids[1]->op != Op::Int || e->kids[1]->value <= 0 || e->kids[1]->value > (1LL << 30)) return false;
+      const int64_t k = e->kids[1]->value;
+      QTerm t;
+      if (!qsingle(e->kids[0], loop_of_var, &t)) return false;
+      if (e->op == Op::FloorDiv) {
+        if (t.mod && t.mod % k) return false;  // (x % m) / k = (x / k) % (m / k) only when k | m
+        if (static_cast<int64_t>(t.div) * k > (1LL << 30)) return false;
+        t.div = static_cast<int32_t>(t.div * k);
+        if (t.mod) t.mod = static_cast<int32_t>(t.mod / k);
+      } else {
+        if (t.mod && t.mod % k) return false;  // (x % m) % k = x % k only when k | m
+        t.mod = static_cast<int32_t>(k);
+      }
+      if (q->n == kQMax) return false;
+      t.coef = scale;
+      q->t[q->n++] = t;
+      return true;
+    }
+    default: return false;
+  }
+}
+
+// AFFCOPY plan for an elementwise block: value = Load or Select(guard, Load, 0)
+// with quasi-affine indices; the guard must be exactly the load's in-bounds
+// predicate (checked like SIMT-A's inlined pad, on corners + 256 samples).
+bool affcopy_plan(const Program& p, const Block& blk, CopyCfg* c) {
+  const Stmt* s = blk.stmt;
+  if (s->init || s->epilogue || blk.loops.empty() || static_cast<int>(blk.loops.size()) > kCopyMaxLoops) return false;
+  const Expr* xl = nullptr;
+  const Expr* cond = nullptr;
+  if (!x_side(s->value, &xl, &cond) || xl->buffer == s->buffer) return false;
+  std::vector<int> loop_of_var(p.vars.size(), -1);
+  c->nl = static_cast<int>(blk.loops.size());
+  c->points = 1;
+  for (int l = 0; l < c->nl; ++l) {
+    const Stmt* L = blk.loops[static_cast<size_t>(l)];
+    if (L->var < 0 || static_cast<size_t>(L->var) >= loop_of_var.size()) return false;
+    loop_of_var[static_cast<size_t>(L->var)] = l;
+    c->ext[l] = L->extent;
+    c->points *= L->extent;
+  }
+  auto strides_of = [&](int buf) {
+    const Buffer& B = p.buffers[static_cast<size_t>(buf)];
+    std::vector<int64_t> st(B.shape.size(), 1);
+    for (size_t d = B.shape.size(); d-- > 1;) st[d - 1] = st[d] * B.shape[d];
+    return st;
+  };
+  auto lin = [&](const std::vector<Expr*>& idx, int buf, QSum* q) {
+    std::vector<int64_t> st = strides_of(buf);
+    *q = QSum();
+    for (size_t d = 0; d < idx.size(); ++d)
+      if (!qdecomp(idx[d], loop_of_var, st[d], q)) return false;
+    return true;
+  };
+  if (!lin(s->indices, s->buffer, &c->out) || !lin(xl->kids, xl->buffer, &c->in)) return false;
+  c->in_buf = xl->buffer;
+  c->out_buf = s->buffer;
+  // guarded dims: with a Select guard every input dim is checked (cheap);
+  // without one the load must be in bounds everywhere (host-sampled below)
+  const Buffer& XB = p.buffers[static_cast<size_t>(xl->buffer)];
+  c->ng = 0;
+  if (cond) {
+    if (xl->kids.size() > static_cast<size_t>(kCopyMaxGuard)) return false;
+    for (size_t d = 0; d < xl->kids.size(); ++d) {
+      c->g[c->ng] = QSum();
+      if (!qdecomp(xl->kids[d], loop_of_var, 1, &c->g[c->ng])) return false;
+      c->gext[c->ng] = XB.shape[d];
+      ++c->ng;
+    }
+  }
+  // host check on corners + 256 samples: the guard is exactly the load's
+  // in-bounds predicate, and an unguarded load never leaves its buffer
+  std::mt19937_64 rng(777);
+  std::vector<int64_t> vals(p.vars.size(), 0);
+  for (int t = 0; t < 258; ++t) {
+    for (const Stmt* L : blk.loops)
+      vals[static_cast<size_t>(L->var)] =
+          t == 0 ? 0 : t == 1 ? L->extent - 1 : static_cast<int64_t>(rng() % static_cast<uint64_t>(L->extent));
+    bool ok = true;
+    bool inb = true;
+    for (size_t d = 0; d < xl->kids.size(); ++d) {
+      int64_t x = host_eval(xl->kids[d], vals, &ok);
+      inb &= x >= 0 && x < XB.shape[d];
+    }
+    if (!ok) return false;
+    if (cond) {
+      int64_t cv = host_eval(cond, vals, &ok);
+      if (!ok || ((cv != 0) != inb)) return false;
+    } else if (!inb) {
+      return false;
+    }
+  }
+  return true;
+}
+
 GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const DeviceLimits& lim) {
   GeneralPlan plan;
   std::string err;
@@ -289,7 +412,7 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
     GStep step;
     step.block = static_cast<int>(bi);
     if (!s->init) {
-      step.family = F_GENERIC;
+      step.family = affcopy_plan(p, blk, &step.copy) ? F_AFFCOPY : F_GENERIC;
       plan.steps.push_back(step);
       continue;
     }

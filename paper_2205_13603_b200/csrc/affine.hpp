@@ -87,6 +87,7 @@ struct GStep {
   bool epilogue_pass = false;
   AffineCfg aff{};
   TcConvCfg conv{};
+  CopyCfg copy{};
   int x_buf = -1, y_buf = -1, c_buf = -1;  // candidate buffer ids (SIMT-A, TC-conv)
 };
 

@@ -103,7 +103,7 @@ __global__ void generic_block_kernel(GenBlock g, const int64_t* __restrict__ cod
         if (vars[i] + 1.0 < (double)g.ext[i]) { vars[i] += 1.0; break; }
         vars[i] = 0.0;
       }
-      if (deadline && (it & 1023) == 1023) {
+      if (deadline && (it & 63) == 63) {  // bytecode iterations are slow: check often
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t > *deadline) { atomicExch(timed_out, 1); return; }
@@ -153,7 +153,7 @@ __global__ void generic_nest_kernel(GenBlock g, const int64_t* __restrict__ code
       if (vars[i] + 1.0 < (double)g.ext[i]) { vars[i] += 1.0; break; }
       vars[i] = 0.0;
     }
-    if (deadline && (it & 1023) == 1023) {
+    if (deadline && (it & 15) == 15) {  // one interpreted iteration costs ~0.1-1 us
       unsigned long long now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now > *deadline) { atomicExch(timed_out, 1); return; }
@@ -161,7 +161,72 @@ __global__ void generic_nest_kernel(GenBlock g, const int64_t* __restrict__ code
   }
 }
 
+// AFFCOPY: thread per point of the block's loops (nest order, last fastest)
+__device__ __forceinline__ int64_t qsum(const QSum& q, const int64_t* lv) {
+  int64_t acc = q.c0;
+  for (int i = 0; i < q.n; ++i) {
+    const QTerm& t = q.t[i];
+    int64_t x = lv[t.loop];
+    if (t.div > 1) x /= t.div;
+    if (t.mod) x %= t.mod;
+    acc += x * t.coef;
+  }
+  return acc;
+}
+
+template <typename Ti, typename To>
+__global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __restrict__ in, To* __restrict__ out) {
+  for (int64_t pt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pt < c.points;
+       pt += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lv[kCopyMaxLoops];
+    int64_t rem = pt;
+    for (int l = c.nl - 1; l >= 0; --l) {
+      const int64_t q = rem / c.ext[l];
+      lv[l] = rem - q * c.ext[l];
+      rem = q;
+    }
+    bool inb = true;
+    for (int d = 0; d < c.ng; ++d) {
+      const int64_t x = qsum(c.g[d], lv);
+      inb &= x >= 0 && x < c.gext[d];
+    }
+    float v = 0.f;
+    if (inb) {
+      const int64_t i = qsum(c.in, lv);
+      if constexpr (sizeof(Ti) == 2) v = __bfloat162float(in[i]);
+      else v = static_cast<float>(in[i]);
+    }
+    const int64_t o = qsum(c.out, lv);
+    if constexpr (sizeof(To) == 2) out[o] = __float2bfloat16_rn(v);
+    else out[o] = v;
+  }
+}
+
 }  // namespace
+
+bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st) {
+  const int ti = B.dtype[c.in_buf], to = B.dtype[c.out_buf];
+  if (ti > 1 || to > 1) return false;
+  const int threads = 256;
+  int64_t blocks = (c.points + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  const void* in = B.ptr[c.in_buf];
+  void* out = B.ptr[c.out_buf];
+  const unsigned nb = static_cast<unsigned>(blocks);
+  if (ti == 0 && to == 0)
+    affcopy_kernel<__nv_bfloat16, __nv_bfloat16><<<nb, threads, 0, st>>>(c, static_cast<const __nv_bfloat16*>(in),
+                                                                        static_cast<__nv_bfloat16*>(out));
+  else if (ti == 0)
+    affcopy_kernel<__nv_bfloat16, float><<<nb, threads, 0, st>>>(c, static_cast<const __nv_bfloat16*>(in),
+                                                                static_cast<float*>(out));
+  else if (to == 0)
+    affcopy_kernel<float, __nv_bfloat16><<<nb, threads, 0, st>>>(c, static_cast<const float*>(in),
+                                                                static_cast<__nv_bfloat16*>(out));
+  else
+    affcopy_kernel<float, float><<<nb, threads, 0, st>>>(c, static_cast<const float*>(in), static_cast<float*>(out));
+  return cudaGetLastError() == cudaSuccess;
+}
 
 bool launch_generic_nest(const GenBlock& g, const int64_t* code, const GenBuffers& B,
                          const unsigned long long* deadline, int* timed_out, cudaStream_t st) {

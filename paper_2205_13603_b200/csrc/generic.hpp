@@ -51,4 +51,29 @@ struct GenProgram {
 
 bool encode_generic(const Program& p, GenProgram* out, std::string* err);
 
+// AFFCOPY: an elementwise stage whose value is a load (optionally behind the
+// load's own in-bounds Select guard, i.e. a pad) whose indices are
+// quasi-affine in the block's loop variables: sums of c * ((v / d) % m)
+// terms, which covers split (affine), fuse (floordiv / mod of the fused
+// variable, `src/schedule.py:374-382`) and their compositions.
+//   out[sum_out] = all guards in range ? in[sum_in] : 0
+constexpr int kCopyMaxLoops = 12;
+constexpr int kCopyMaxGuard = 4;
+constexpr int kQMax = 16;
+struct QTerm { int32_t loop, div, mod, pad; int64_t coef; };
+struct QSum {
+  int n = 0;
+  int64_t c0 = 0;
+  QTerm t[kQMax];
+};
+struct CopyCfg {
+  int nl = 0, ng = 0;
+  int in_buf = -1, out_buf = -1;
+  int64_t ext[kCopyMaxLoops] = {0};
+  QSum out, in;                 // element offsets
+  QSum g[kCopyMaxGuard];        // guarded input dims (index values)
+  int64_t gext[kCopyMaxGuard] = {0};
+  int64_t points = 1;
+};
+
 }  // namespace lsb

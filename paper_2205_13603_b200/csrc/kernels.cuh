@@ -37,6 +37,8 @@ void launch_parity(float* c, const double* ref, int64_t n, double rtol, double a
 // clamp(factor * best, floor, cap) (cap while nothing has succeeded yet).
 void launch_arm(unsigned long long* state, const int* prev_flag, const unsigned long long* prev_parity,
                 double factor, unsigned long long floor_ns, unsigned long long cap_ns, cudaStream_t st);
+// end stamp of a candidate's checked launches: state[3] = now
+void launch_stamp(unsigned long long* state, cudaStream_t st);
 // spin on the device for ~ns (lets the host queue a chunk of launches)
 void launch_delay(unsigned long long ns, cudaStream_t st);
 // fp32 -> bf16 copy, and an optional 2-D transpose to make K contiguous

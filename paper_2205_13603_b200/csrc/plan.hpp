@@ -54,7 +54,7 @@ struct Workload {
 
 bool analyze_workload(const Program& e0, Workload* w, std::string* err);
 
-enum Family { F_NONE = 0, F_NAIVE = 1, F_SIMT = 2, F_TC = 3, F_LOOPNEST = 4, F_GENERIC = 5, F_NESTGEN = 6, F_SIMTA = 7, F_TCCONV = 8 };
+enum Family { F_NONE = 0, F_NAIVE = 1, F_SIMT = 2, F_TC = 3, F_LOOPNEST = 4, F_GENERIC = 5, F_NESTGEN = 6, F_SIMTA = 7, F_TCCONV = 8, F_AFFCOPY = 9 };
 enum PlanStatus { P_OK = 0, P_ILLEGAL = 1, P_UNSUPPORTED = 2, P_PARSE = 3 };
 
 struct Part { int role; int64_t extent; int64_t stride; Kind kind; };

@@ -143,19 +143,48 @@ struct ls_runner {
   DeviceLimits lim;
   double launch_host_us = 4.0;  // host enqueue cost per call, for sizing the device spin
 
+  // Device memory pool for per-workload buffers: set_workload is called once
+  // per task (and per bench step); reusing same-size blocks avoids
+  // cudaMalloc/cudaFree (implicitly synchronising, ~ms) on every call.
+  std::multimap<size_t, void*> pool_free;
+  std::map<void*, size_t> pool_size;
+  cudaError_t pmalloc(void** p, size_t n) {
+    n = (n + 255) & ~static_cast<size_t>(255);
+    auto it = pool_free.lower_bound(n);
+    if (it != pool_free.end() && it->first <= 2 * n) {
+      *p = it->second;
+      pool_free.erase(it);
+      return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(p, n);
+    if (e == cudaSuccess) pool_size[*p] = n;
+    return e;
+  }
+  void pfree(void* p) {
+    if (!p) return;
+    auto it = pool_size.find(p);
+    if (it == pool_size.end()) { cudaFree(p); return; }
+    pool_free.emplace(it->second, p);
+  }
+  void pool_release() {
+    for (auto& kv : pool_size) cudaFree(kv.first);
+    pool_size.clear();
+    pool_free.clear();
+  }
+
   ~ls_runner() { release(); }
 
   void release_workload() {
     for (size_t i = 0; i < gbuf.size(); ++i)
-      if (gbuf[i] != c) cudaFree(gbuf[i]);
+      if (gbuf[i] != c) pfree(gbuf[i]);
     gbuf.clear();
-    cudaFree(wt);
+    pfree(wt);
     wt = nullptr;
     tmap_wt.clear();
     tmap_x.clear();
     gbuf_dtype.clear();
     general = false;
-    cudaFree(x); cudaFree(y); cudaFree(yk); cudaFree(c); cudaFree(ref);
+    pfree(x); pfree(y); pfree(yk); pfree(c); pfree(ref);
     x = y = yk = nullptr; c = nullptr; ref = nullptr;
     tmap_b.clear();
     tmap_am.clear();
@@ -167,6 +196,7 @@ struct ls_runner {
     if (st) cudaStreamSynchronize(st);
     release_workload();
     cudaFree(deadline); cudaFree(flags); cudaFree(parity); cudaFree(gcode); cudaFree(tcsync);
+    pool_release();
     gcode = nullptr;
     tcsync = nullptr;
     tcsync_cap = 0;
@@ -295,6 +325,8 @@ struct ls_runner {
         const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
         if (!mx || !mw) return false;
         ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st);
+      } else if (stp.family == F_AFFCOPY) {
+        ok = launch_affcopy(stp.copy, B, st);
       } else if (stp.family == F_SIMTA) {
         ok = launch_simta(B.ptr[stp.x_buf], B.ptr[stp.y_buf], static_cast<float*>(B.ptr[stp.c_buf]), stp.aff, bf16, dl,
                           flag, st);
@@ -437,14 +469,14 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     for (int64_t x : gw.shapes[b]) elems *= x;
     const size_t n = static_cast<size_t>(elems);
     if (gw.roles[b] == 0) {  // input: runner dtype, shared by the reference run
-      LSB_CUDA(cudaMalloc(&r->gbuf[b], n * es));
+      LSB_CUDA(r->pmalloc(&r->gbuf[b], n * es));
       if (r->bf16) {
         float* tmp = nullptr;
-        LSB_CUDA(cudaMalloc(&tmp, n * 4));
+        LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&tmp), n * 4));
         LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[inp], n * 4, cudaMemcpyHostToDevice, r->st));
         launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(r->gbuf[b]), elems, r->st);
         LSB_CUDA(cudaStreamSynchronize(r->st));
-        cudaFree(tmp);
+        r->pfree(tmp);
       } else {
         LSB_CUDA(cudaMemcpyAsync(r->gbuf[b], host_inputs[inp], n * 4, cudaMemcpyHostToDevice, r->st));
       }
@@ -452,22 +484,22 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
       refbuf[b] = r->gbuf[b];
       refdt[b] = r->gbuf_dtype[b];
     } else if (gw.roles[b] == 1 && gw.buffers[b] == gw.c_buf) {  // contraction output
-      LSB_CUDA(cudaMalloc(&r->c, n * 4));
-      LSB_CUDA(cudaMalloc(&r->ref, n * 8));
+      LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->c), n * 4));
+      LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->ref), n * 8));
       r->gbuf[b] = r->c;
       r->gbuf_dtype[b] = 1;
       refbuf[b] = r->ref;
     } else if (gw.roles[b] == 1) {  // the final output of a later stage (e.g. relu)
-      LSB_CUDA(cudaMalloc(&r->c, n * 4));
-      LSB_CUDA(cudaMalloc(&r->ref, n * 8));
+      LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->c), n * 4));
+      LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->ref), n * 8));
       r->gbuf[b] = r->c;
       r->gbuf_dtype[b] = 1;
       r->w.c_elems = elems;
       refbuf[b] = r->ref;
     } else {  // intermediate: fp32 when it holds the contraction's sums, else runner dtype
       if (gw.buffers[b] == gw.c_buf) r->gbuf_dtype[b] = 1;
-      LSB_CUDA(cudaMalloc(&r->gbuf[b], n * (r->gbuf_dtype[b] == 1 ? 4 : es)));
-      LSB_CUDA(cudaMalloc(&refbuf[b], n * 8));
+      LSB_CUDA(r->pmalloc(&r->gbuf[b], n * (r->gbuf_dtype[b] == 1 ? 4 : es)));
+      LSB_CUDA(r->pmalloc(&refbuf[b], n * 8));
       temps.push_back(refbuf[b]);
     }
   }
@@ -489,7 +521,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     }
   LSB_CUDA(cudaStreamSynchronize(r->st));
   cudaFree(code);
-  for (void* t : temps) cudaFree(t);
+  for (void* t : temps) r->pfree(t);
   // K-major weight copy for the tcgen05 conv family: the contraction's
   // weight viewed as [k_rows][n_cols] (n = its contiguous last dim)
   r->tc_ok = false;
@@ -502,7 +534,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     r->wt_cols = sh.back();
     r->wt_rows = elems / r->wt_cols;
     if (r->wt_rows % 64 || r->wt_cols % 16) break;
-    LSB_CUDA(cudaMalloc(&r->wt, static_cast<size_t>(elems) * 2));
+    LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 2));
     launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
                           r->wt_rows, r->wt_cols, r->st);
     LSB_CUDA(cudaGetLastError());
@@ -650,24 +682,24 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
       set_error("operand is not an input buffer");
       return LS_ERR_ARG;
     }
-    LSB_CUDA(cudaMalloc(dst, static_cast<size_t>(elems) * es));
+    LSB_CUDA(r->pmalloc(dst, static_cast<size_t>(elems) * es));
     if (!r->bf16) {
       LSB_CUDA(cudaMemcpyAsync(*dst, host_inputs[idx], static_cast<size_t>(elems) * 4, cudaMemcpyHostToDevice, r->st));
     } else {
       float* tmp = nullptr;
-      LSB_CUDA(cudaMalloc(&tmp, static_cast<size_t>(elems) * 4));
+      LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&tmp), static_cast<size_t>(elems) * 4));
       LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[idx], static_cast<size_t>(elems) * 4, cudaMemcpyHostToDevice, r->st));
       launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(*dst), elems, r->st);
       LSB_CUDA(cudaStreamSynchronize(r->st));
-      cudaFree(tmp);
+      r->pfree(tmp);
     }
     return LS_OK;
   };
   ls_status s;
   if ((s = upload(w.x_buf, w.x_elems, &r->x)) != LS_OK) return s;
   if ((s = upload(w.y_buf, w.y_elems, &r->y)) != LS_OK) return s;
-  LSB_CUDA(cudaMalloc(&r->c, static_cast<size_t>(w.c_elems) * 4));
-  LSB_CUDA(cudaMalloc(&r->ref, static_cast<size_t>(w.c_elems) * 8));
+  LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->c), static_cast<size_t>(w.c_elems) * 4));
+  LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->ref), static_cast<size_t>(w.c_elems) * 8));
   launch_reference(r->x, r->y, r->ref, r->s, r->bf16, r->st);
   LSB_CUDA(cudaGetLastError());
 
@@ -682,10 +714,10 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
   if (r->tc_ok) {
     if (y_kmaj) {
       r->yk = nullptr;
-      LSB_CUDA(cudaMalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
+      LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
       LSB_CUDA(cudaMemcpyAsync(r->yk, r->y, static_cast<size_t>(w.y_elems) * 2, cudaMemcpyDeviceToDevice, r->st));
     } else {
-      LSB_CUDA(cudaMalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
+      LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
       launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->y), static_cast<__nv_bfloat16*>(r->yk), B, K, N,
                             r->st);
       LSB_CUDA(cudaGetLastError());
@@ -768,7 +800,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   // element a candidate fails to write is a mismatch.  The deadline of each
   // checked launch is armed on the device from the best time seen so far.
   std::vector<char> launched(static_cast<size_t>(n), 0);
-  const unsigned long long best_init[3] = {0, 0, ~0ull};
+  const unsigned long long best_init[4] = {0, 0, ~0ull, 0};
   LSB_CUDA(cudaMemcpyAsync(r->deadline, best_init, sizeof best_init, cudaMemcpyHostToDevice, r->st));
   LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
   const unsigned long long floor_ns = static_cast<unsigned long long>(r->opts.timeout_floor_ms * 1e6);
@@ -799,6 +831,8 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     LSB_CUDA(cudaEventRecord(E[4 * i], r->st));
     bool ok = r->launch(p, true, i);
     LSB_CUDA(cudaEventRecord(E[4 * i + 1], r->st));
+    launch_stamp(r->deadline, r->st);
+    ++r->launches;
     if (!ok) {
       cudaGetLastError();
       out[i].status = LS_RUN_LAUNCH;

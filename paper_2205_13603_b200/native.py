@@ -105,7 +105,7 @@ EXPORTS = {
 STATUS = {0: "OK", 1: "ILLEGAL", 2: "UNSUPPORTED", 3: "PARSE", 4: "LAUNCH", 5: "PARITY",
           6: "TIMEOUT"}
 FAMILY = {0: "none", 1: "naive", 2: "simt", 3: "tcgen05", 4: "loopnest", 5: "generic", 6: "nestgen",
-          7: "simt_affine", 8: "tcgen05_conv"}
+          7: "simt_affine", 8: "tcgen05_conv", 9: "affcopy"}
 
 
 class NativeError(RuntimeError):

@@ -222,6 +222,21 @@ def test_conv2d_general_path_bit_exact(dtype):
     r.close()
 
 
+def test_conv2d_population_slice_has_no_parity_failures():
+    # a bench-sized slice through every general-path family (AFFCOPY pad
+    # stages incl. fused/vectorised pad loops, SIMT-A, NESTGEN, tcgen05 conv):
+    # the in-run parity reducer flags no candidate
+    hdr, pop = load_population("conv2d")
+    e0 = hdr["e0"]
+    r = make_runner("bf16", timeout_ms=5.0, timeout_factor=10.0)
+    r.set_workload(e0, seed=0)
+    res = r.measure_programs([p["program"] for p in pop[:384]])
+    bad = [x for x in res if x["status"] in ("PARITY", "LAUNCH")]
+    assert not bad, bad[:3]
+    assert sum(x["status"] == "OK" for x in res) > 50
+    r.close()
+
+
 def test_dense_relu_general_path_exact():
     from paper_2205_13603_b200.inputs import random_inputs as ri
     import gzip
