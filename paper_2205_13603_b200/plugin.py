@@ -135,3 +135,29 @@ def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
             raise ValueError(f"unknown mode {mode!r}")
     with installed(runner, scorer):
         return ls.search.tune(e0, generator, config, machine_spec, warm_records)
+
+
+def tune_with_records(e0, generator, config=None, machine_spec=None, *, runner=None, scorer=None,
+                      mode: str = "hardware", records_path=None, warm_path=None, device: int = 0,
+                      dtype: str = "bf16", peak_tflops=None, peak_source="", **runner_opts):
+    """``tune`` plus the hardware record/report format (records.py): warm-starts
+    from ``warm_path`` (records of the same workload and unit only), writes the
+    log to ``records_path`` and returns ``(report, report_json)`` where the JSON
+    is the reference's report with a ``hardware`` section (best-schedule
+    TFLOPS, roofline fraction, per-record kernel family / configuration)."""
+    from . import records as R
+    unit = "cycles" if mode == "parity" else "ns"
+    ctx = R.HardwareContext.for_workload(e0, unit=unit, dtype=dtype, peak_tflops=peak_tflops,
+                                         peak_source=peak_source)
+    warm = R.load_records(warm_path, workload_hash=ctx.workload_hash, unit=unit) if warm_path else None
+    if runner is None and mode == "hardware":
+        from .runner import B200Runner
+        runner = B200Runner(device=device, dtype=dtype, **runner_opts)
+        runner.set_workload(e0)
+    rec = R.RecordingRunner(runner) if runner is not None else None
+    report = tune(e0, generator, config, machine_spec, warm, mode=mode, runner=rec, scorer=scorer,
+                  device=device, dtype=dtype)
+    info = rec.info if rec is not None else {}
+    if records_path:
+        R.save_records(records_path, report.log, ctx, info)
+    return report, R.report_json(report, ctx, info)
