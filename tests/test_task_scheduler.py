@@ -1,0 +1,63 @@
+"""Whole-network trial allocation (task_scheduler.py) on
+scaled-down BERT tasks, driving the reference's own tune on CPU."""
+import pytest
+
+from conftest import needs_reference
+
+pytestmark = needs_reference
+
+
+def ref_tune():
+    from paper_2205_13603_b200.refapi import loopsched
+    ls = loopsched()
+    return lambda e0, gen, cfg, warm: ls.tune(e0, gen, cfg, ls.MachineSpec(), warm)
+
+
+def make(total, seed=0, scale=16, round_trials=16):
+    from paper_2205_13603_b200.task_scheduler import TaskScheduler, bert_tasks
+    tasks = bert_tasks(seq=128, layers=12, scale=scale)
+    return TaskScheduler(tasks, total, round_trials=round_trials, batch=8, population=16, seed=seed,
+                         tune_fn=ref_tune())
+
+
+def test_bert_task_extraction_full_size():
+    from paper_2205_13603_b200.task_scheduler import bert_tasks
+    from paper_2205_13603_b200.records import contraction_flops
+    tasks = bert_tasks()
+    assert [t.name for t in tasks] == ["dense_qkvo", "ffn_in", "ffn_out", "attn_qk", "attn_pv"]
+    assert [t.weight for t in tasks] == [48, 12, 12, 12, 12]
+    # 1.862 GFLOP per layer, 22.35 GFLOP for 12 layers
+    per_layer = sum(contraction_flops(t.e0) * t.weight / 12 for t in tasks)
+    assert per_layer == pytest.approx(1.862e9, rel=1e-3)
+
+
+def test_budget_warmup_and_determinism():
+    a = make(112, seed=3)
+    s = a.run()
+    assert s["trials"] <= 112
+    assert all(t["rounds"] >= 1 for t in s["tasks"])          # warm-up round for every task
+    assert s["objective"] is not None and s["speedup"] >= 1.0
+    b = make(112, seed=3).run()
+    assert [r["task"] for r in s["allocation"]] == [r["task"] for r in b["allocation"]]
+    assert s["objective_exact"] == b["objective_exact"]
+
+
+def test_objective_is_weighted_best_and_monotone():
+    from fractions import Fraction
+    sch = make(128, seed=1)
+    sch.run()
+    assert sch.objective() == sum(Fraction(t.weight) * t.best for t in sch.tasks)
+    for t in sch.tasks:
+        bests = [b for _, b in t.history]
+        assert all(x >= y for x, y in zip(bests, bests[1:]))  # per-task best never regresses
+        assert t.best <= t.baseline
+
+
+def test_gradient_prefers_heavier_identical_task():
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.task_scheduler import Task, TaskScheduler
+    ls = loopsched()
+    tasks = [Task("light", ls.gmm(16, 48, 48), 1), Task("heavy", ls.gmm(16, 48, 48), 16)]
+    sch = TaskScheduler(tasks, 96, round_trials=16, batch=8, population=16, seed=5, tune_fn=ref_tune())
+    sch.run()
+    assert tasks[1].trials > tasks[0].trials
