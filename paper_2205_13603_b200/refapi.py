@@ -2,8 +2,11 @@
 
 The B200 path plugs into the reference's own seams; the
 reference itself is never copied or edited.  It is imported from the normal
-module path, or from ``$LOOPSCHED_SRC`` / ``/root/reference/pkg/src`` when that
-directory exists.  On a GPU box without the reference, everything that only
+module path, or from ``$LOOPSCHED_SRC``, the unmodified install under
+``baseline/_ref`` (``pip install --no-deps --target baseline/_ref`` of the
+reference package; git-ignored, it travels to the GPU box with the repo
+snapshot) or ``/root/reference/pkg/src`` when that directory exists.  Without
+any of them, everything that only
 consumes serialized programs (runner, scorer, simulator) still works; only the
 search-side helpers (builders, transformation modules, ``tune`` wrapper) need
 this module.
@@ -15,7 +18,9 @@ import importlib
 import os
 import sys
 
-_CANDIDATE_DIRS = (os.environ.get("LOOPSCHED_SRC", ""), "/root/reference/pkg/src")
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_CANDIDATE_DIRS = (os.environ.get("LOOPSCHED_SRC", ""), os.path.join(_ROOT, "baseline", "_ref"),
+                   "/root/reference/pkg/src")
 
 
 def loopsched():

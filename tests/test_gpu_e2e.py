@@ -1,0 +1,54 @@
+"""End to end on the B200: the reference's unchanged ``tune`` with the B200
+seams installed (plugin.py).  Needs the reference package importable (the
+unmodified install under baseline/_ref travels with the repo snapshot)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, needs_reference
+
+pytestmark = [pytest.mark.gpu, needs_reference]
+
+
+def test_parity_mode_tune_equals_reference_report():
+    # K8 exact latencies + K7 features/scores inside the reference search:
+    # the whole report (every measured trace, the chosen best trace, the
+    # refitted model's statistics) equals the CPU reference's, seed 0
+    from paper_2205_13603_b200 import plugin
+    from paper_2205_13603_b200.refapi import loopsched
+    ls = loopsched()
+    want = json.load(open(os.path.join(GOLDEN, "tune_gmm512.json")))
+    report = plugin.tune(ls.gmm(512, 512, 512), ls.default_space(),
+                         ls.SearchConfig(trials=64, batch=16, population=64, seed=0), mode="parity")
+    got = report.to_json(timestamp=False)
+    for k in ("baseline", "best", "rounds", "exhausted", "trials"):
+        assert got[k] == want[k], k
+    # every measured trace, in order, with its exact latency; K7 features
+    # within 1e-14 (CUDA log1p vs libm, SURVEY.md §8c tolerance 1e-5)
+    assert len(got["log"]) == len(want["log"])
+    for g, w in zip(got["log"], want["log"]):
+        assert (g["hash"], g["exact"], g["trace"]) == (w["hash"], w["exact"], w["trace"])
+        np.testing.assert_allclose(g["features"], w["features"], rtol=1e-14, atol=0)
+
+
+def test_hardware_mode_tune_reports_tflops(tmp_path):
+    # hardware latencies (ns Fractions) from the B200 Runner drive the same
+    # search; the report carries best-schedule TFLOPS and the records reload
+    from paper_2205_13603_b200 import plugin, records as R
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.tensor_core import b200_space
+    ls = loopsched()
+    e0 = ls.gmm(128, 768, 3072)
+    report, doc = plugin.tune_with_records(e0, b200_space(), ls.SearchConfig(trials=32, batch=16, population=32,
+                                                                             seed=0),
+                                           mode="hardware", records_path=str(tmp_path / "r.jsonl"),
+                                           peak_tflops=1668.5, timeout_ms=2.0, min_repeats=3, max_repeats=20,
+                                           target_ms=0.05)
+    assert report.best is not None and len(report.log) == 32
+    hw = doc["hardware"]
+    assert hw["context"]["unit"] == "ns" and hw["best"]["tflops"] > 1.0
+    assert report.best.latency < report.baseline_latency
+    back = R.load_records(str(tmp_path / "r.jsonl"), unit="ns")
+    assert [b.latency for b in back] == [r.latency for r in report.log]
