@@ -260,6 +260,7 @@ bool tc_conv_plan(const GeneralWorkload& w, const Program& p, const Stmt* s, con
     if (cc[v] % 4) return false;  // float4 epilogue stores
   }
   if (t.c0 % 4 || t.cc_h1 % 4 || t.cc_w1 % 4) return false;
+  if (t.splits * t.kt > kConvMaxK) return false;  // per-k-tile coordinate table (tc_conv.cu)
   const int64_t stage = 128 * 64 * 2 + t.bn * 64 * 2;
   const bool cluster = t.splits > 1;
   const int64_t rows_per = (64 + t.splits - 1) / t.splits;

@@ -67,6 +67,7 @@ struct AffineCfg {
 // k-tile.  Per-part contributions to the TMA coordinates of the 4-D X-side
 // box (n, h, w, c), to the flattened K index of the K-major weight copy, and
 // to the output address.
+constexpr int kConvMaxK = 64;  // splits x k-tiles of one tcgen05 conv candidate
 struct CList {
   int n;
   int64_t ext[8], xn[8], xh[8], xw[8], xc[8], kf[8], cc[8], co[8];

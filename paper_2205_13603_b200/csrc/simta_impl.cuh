@@ -22,12 +22,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// digits of idx over the parts of one list (nest order, last fastest)
-__device__ __forceinline__ void decode(const AList& L, int64_t idx, int64_t* sx, int64_t* sy, int64_t* sc,
+// digits of idx over the parts of one list (nest order, last fastest); the
+// indices and extents fit in 32 bits, and 32-bit division is ~4x cheaper
+__device__ __forceinline__ void decode(const AList& L, int64_t idx64, int64_t* sx, int64_t* sy, int64_t* sc,
                                        int64_t* g0, int64_t* g1) {
+  uint32_t idx = static_cast<uint32_t>(idx64);
   for (int p = L.n - 1; p >= 0; --p) {
-    const int64_t d = idx % L.ext[p];
-    idx /= L.ext[p];
+    const uint32_t e = static_cast<uint32_t>(L.ext[p]);
+    const uint32_t q = idx / e;
+    const int64_t d = static_cast<int64_t>(idx - q * e);
+    idx = q;
     *sx += d * L.cx[p];
     *sy += d * L.cy[p];
     *sc += d * L.cc[p];

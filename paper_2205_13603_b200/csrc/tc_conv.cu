@@ -34,9 +34,19 @@ constexpr int kLiveA = 64 * 64 * 2;    // bytes TMA writes per A stage
 constexpr int kRows = 64;
 constexpr int kMaxClusterSplits = 16;
 
+// X-box / weight-K coordinates of one (split, k-tile) pair, relative to the
+// CTA origin; precomputed on the host so the TMA producer does one table
+// lookup per k-tile (the mixed-radix decode of the k parts used to cost the
+// single producer thread ~1000 cycles of 64-bit division per k-tile).
+struct KCoord {
+  int32_t c, w, h, n, kf, pad;
+};
+
 struct TcConvArgs {
   float* c;
-  TcConvCfg g;
+  CList m_grid, n_grid;       // origin parts of the output-pixel box and channel tile
+  int64_t x_n0, x_h0, x_w0, x_c0, c0, cc_h1, cc_w1;
+  KCoord kc[kConvMaxK];       // [split * kt + k-tile]
   int bn, splits, kt, stages, mode;
   uint32_t idesc, tmem_cols;
 };
@@ -45,7 +55,24 @@ struct Coord {
   int64_t n, h, w, c, kf, co, cc;
 };
 
-__device__ __forceinline__ void add_parts(const CList& L, int64_t idx, Coord& a) {
+// origin decode: 32-bit mixed radix (grid indices and extents fit in int32)
+__device__ __forceinline__ void add_parts(const CList& L, uint32_t idx, Coord& a) {
+  for (int i = L.n - 1; i >= 0; --i) {
+    const uint32_t e = static_cast<uint32_t>(L.ext[i]);
+    const uint32_t q = idx / e;
+    const int64_t v = static_cast<int64_t>(idx - q * e);
+    idx = q;
+    a.n += v * L.xn[i];
+    a.h += v * L.xh[i];
+    a.w += v * L.xw[i];
+    a.c += v * L.xc[i];
+    a.kf += v * L.kf[i];
+    a.co += v * L.co[i];
+    a.cc += v * L.cc[i];
+  }
+}
+
+void host_add_parts(const CList& L, int64_t idx, Coord& a) {
   for (int i = L.n - 1; i >= 0; --i) {
     const int64_t v = idx % L.ext[i];
     idx /= L.ext[i];
@@ -111,10 +138,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
 
   // tile origin: output-pixel box (grid y), channel tile (grid x), split (grid z)
-  Coord o{a.g.x_n0, a.g.x_h0, a.g.x_w0, a.g.x_c0, 0, 0, a.g.c0};
-  add_parts(a.g.m_grid, blockIdx.y, o);
-  add_parts(a.g.n_grid, blockIdx.x, o);
-  add_parts(a.g.k_split, blockIdx.z, o);
+  Coord o{a.x_n0, a.x_h0, a.x_w0, a.x_c0, 0, 0, a.c0};
+  add_parts(a.m_grid, blockIdx.y, o);
+  add_parts(a.n_grid, blockIdx.x, o);
+  const KCoord* kc = a.kc + blockIdx.z * a.kt;
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -126,12 +153,11 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       const int s = kt % a.stages;
       const uint32_t ph = (kt / a.stages) & 1;
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
-      Coord t = o;
-      add_parts(a.g.k_tile, kt, t);
+      const KCoord k = kc[kt];
       mbar_expect_tx(full + 8 * s, stage_bytes);
-      tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(t.c), static_cast<int>(t.w),
-                  static_cast<int>(t.h), static_cast<int>(t.n));
-      tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(t.kf), static_cast<int>(t.co), 0);
+      tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c, static_cast<int>(o.w) + k.w,
+                  static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n);
+      tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf, static_cast<int>(o.co), 0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
@@ -156,7 +182,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const int row = warp * 32 + lane;
   const int c4 = a.bn / 4;
   float* cbase = a.c + o.cc;
-  auto out_row = [&](int r) { return cbase + (r >> 3) * a.g.cc_h1 + (r & 7) * a.g.cc_w1; };
+  auto out_row = [&](int r) { return cbase + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1; };
   if (a.mode == 1) {
     const uint32_t me = cluster_rank();
     if (warp < 2) {
@@ -221,9 +247,26 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
   if (g.splits > kMaxClusterSplits || g.grid_m > 65535 || g.grid_n > 65535) return false;
+  if (g.splits * g.kt > kConvMaxK) return false;
   TcConvArgs a;
   a.c = c;
-  a.g = g;
+  a.m_grid = g.m_grid;
+  a.n_grid = g.n_grid;
+  a.x_n0 = g.x_n0; a.x_h0 = g.x_h0; a.x_w0 = g.x_w0; a.x_c0 = g.x_c0;
+  a.c0 = g.c0; a.cc_h1 = g.cc_h1; a.cc_w1 = g.cc_w1;
+  for (int64_t sp = 0; sp < g.splits; ++sp)
+    for (int64_t kt = 0; kt < g.kt; ++kt) {
+      Coord t{0, 0, 0, 0, 0, 0, 0};
+      host_add_parts(g.k_split, sp, t);
+      host_add_parts(g.k_tile, kt, t);
+      KCoord& k = a.kc[sp * g.kt + kt];
+      k.c = static_cast<int32_t>(t.c);
+      k.w = static_cast<int32_t>(t.w);
+      k.h = static_cast<int32_t>(t.h);
+      k.n = static_cast<int32_t>(t.n);
+      k.kf = static_cast<int32_t>(t.kf);
+      k.pad = 0;
+    }
   a.bn = static_cast<int>(g.bn);
   a.splits = static_cast<int>(g.splits);
   a.kt = static_cast<int>(g.kt);
