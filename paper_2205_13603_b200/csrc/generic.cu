@@ -103,7 +103,7 @@ __global__ void generic_block_kernel(GenBlock g, const int64_t* __restrict__ cod
         if (vars[i] + 1.0 < (double)g.ext[i]) { vars[i] += 1.0; break; }
         vars[i] = 0.0;
       }
-      if (deadline && (it & 63) == 63) {  // bytecode iterations are slow: check often
+      if (deadline && (it & 7) == 7) {  // bytecode iterations are slow: check often
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t > *deadline) { atomicExch(timed_out, 1); return; }
@@ -153,7 +153,7 @@ __global__ void generic_nest_kernel(GenBlock g, const int64_t* __restrict__ code
       if (vars[i] + 1.0 < (double)g.ext[i]) { vars[i] += 1.0; break; }
       vars[i] = 0.0;
     }
-    if (deadline && (it & 15) == 15) {  // one interpreted iteration costs ~0.1-1 us
+    if (deadline) {  // one interpreted iteration costs ~1-10 us: check every one
       unsigned long long now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now > *deadline) { atomicExch(timed_out, 1); return; }

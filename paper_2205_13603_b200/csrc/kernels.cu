@@ -208,6 +208,14 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
       }
       __syncthreads();
     }
+    if (a.deadline) {  // finished past the deadline: a timeout (no timed repeats)
+      if (tid == 0) abort_flag = gtimer() > *a.deadline;
+      __syncthreads();
+      if (abort_flag) {
+        if (tid == 0) atomicExch(a.timed_out, 1);
+        return;
+      }
+    }
     const int64_t b = b0 + tb_i * a.rb + rbi;
     float* crow = c + b * s.sc[0] + (m0 + tm_i * RM) * s.sc[1] + (n0 + tn_i * RN) * s.sc[2];
 #pragma unroll
@@ -257,7 +265,7 @@ __global__ void loopnest_contract(const T* __restrict__ x, const T* __restrict__
       idx[l] = 0;
       ox -= L.dx[l] * (L.ext[l] - 1); oy -= L.dy[l] * (L.ext[l] - 1); oc -= L.dc[l] * (L.ext[l] - 1);
     }
-    if (a.deadline && (it & 4095) == 4095 && gtimer() > *a.deadline) {
+    if (a.deadline && (it & 255) == 255 && gtimer() > *a.deadline) {
       atomicExch(a.timed_out, 1);
       return;
     }
@@ -295,6 +303,7 @@ __global__ void arm_kernel(unsigned long long* s, const int* prev_flag, const un
     // s[3]: end stamp of the previous candidate's kernels (launch_stamp), so
     // host enqueue gaps between candidates do not inflate the best time
     unsigned long long el = (s[3] > s[1] ? s[3] : now) - s[1];
+    el = el > s[4] ? el - s[4] : 0;  // minus the calibrated empty-candidate overhead
     if (el < s[2]) s[2] = el;
   }
   unsigned long long t = cap_ns;

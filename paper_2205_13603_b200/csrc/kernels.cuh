@@ -31,7 +31,8 @@ void launch_loopnest(const void* x, const void* y, float* c, const LoopNestCfg& 
 // so a later candidate that skips an element fails its own check.
 void launch_parity(float* c, const double* ref, int64_t n, double rtol, double atol, unsigned long long* slot,
                    bool poison, cudaStream_t st);
-// Device-side deadline state: [0] deadline, [1] arm time, [2] best elapsed ns.
+// Device-side deadline state: [0] deadline, [1] arm time, [2] best elapsed ns,
+// [3] end stamp of the last candidate, [4] calibrated empty-candidate ns.
 // arm: first settles the previous candidate (its elapsed time updates best
 // when it neither timed out nor failed parity), then sets deadline = now +
 // clamp(factor * best, floor, cap) (cap while nothing has succeeded yet).

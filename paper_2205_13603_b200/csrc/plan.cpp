@@ -1,4 +1,5 @@
 // Trace-to-kernel instantiator.  See plan.hpp for the mapping convention.
+#include <cstdlib>
 #include "plan.hpp"
 
 #include <algorithm>
@@ -242,7 +243,8 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles, t.grid_n, lim.max_smem);
       int64_t avail = lim.max_smem - 1024 - 256 - g0.recv;
       t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / g0.stage_bytes));
-      t.stages = std::min<int64_t>(t.stages, 8);
+      static const int64_t max_stages = getenv("LSB_TC_MAXSTAGES") ? atoi(getenv("LSB_TC_MAXSTAGES")) : 8;
+      t.stages = std::min<int64_t>(t.stages, std::max<int64_t>(1, max_stages));
       TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles, t.grid_n, lim.max_smem);
       plan.needs_zero = g.mode == 3;
       t.direct = g.direct;

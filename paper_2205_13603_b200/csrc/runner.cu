@@ -142,6 +142,7 @@ struct ls_runner {
   double stats[8] = {0};  // host ms phase A, host ms phase B, spin us, phase-B launches
   DeviceLimits lim;
   double launch_host_us = 4.0;  // host enqueue cost per call, for sizing the device spin
+  unsigned long long empty_ns = 0;  // device elapsed of an empty candidate (arm -> stamp), calibrated
 
   // Device memory pool for per-workload buffers: set_workload is called once
   // per task (and per bench step); reusing same-size blocks avoids
@@ -629,9 +630,30 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   r->lim.max_threads = prop.maxThreadsPerBlock;
   r->lim.max_smem = static_cast<int64_t>(prop.sharedMemPerBlockOptin) - 1024;
   LSB_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
-  LSB_CUDA(cudaMalloc(&r->deadline, 4 * sizeof(unsigned long long)));
+  LSB_CUDA(cudaMalloc(&r->deadline, 8 * sizeof(unsigned long long)));
   ls_status s = r->ensure_capacity(256);
   if (s != LS_OK) return s;
+  // calibrate the device-side elapsed time of an empty candidate (arm kernel,
+  // event, stamp kernel: the launch gaps a real candidate's elapsed time also
+  // carries), so the best-so-far behind every deadline is the kernel time
+  {
+    unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, 0, 0};
+    LSB_CUDA(cudaMemcpy(r->deadline, init, sizeof init, cudaMemcpyHostToDevice));
+    cudaEvent_t e;
+    LSB_CUDA(cudaEventCreate(&e));
+    unsigned long long best = ~0ull;
+    for (int i = 0; i < 16; ++i) {
+      launch_arm(r->deadline, nullptr, nullptr, 0.0, 0, 0, r->st);
+      LSB_CUDA(cudaEventRecord(e, r->st));
+      launch_stamp(r->deadline, r->st);
+      unsigned long long h[4];
+      LSB_CUDA(cudaMemcpyAsync(h, r->deadline, sizeof h, cudaMemcpyDeviceToHost, r->st));
+      LSB_CUDA(cudaStreamSynchronize(r->st));
+      if (h[3] > h[1]) best = std::min(best, h[3] - h[1]);
+    }
+    cudaEventDestroy(e);
+    r->empty_ns = best == ~0ull ? 0 : best;
+  }
   *out = r.release();
   return LS_OK;
 }
@@ -794,13 +816,14 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   auto host_now = [] { return std::chrono::duration<double, std::milli>(
                             std::chrono::steady_clock::now().time_since_epoch()).count(); };
   std::memset(r->stats, 0, sizeof r->stats);
+  r->stats[4] = static_cast<double>(r->empty_ns) / 1e3;
   double h0 = host_now();
   // ---- phase A: checked run ----
   // C starts poisoned (NaN) and the parity reducer re-poisons it, so any
   // element a candidate fails to write is a mismatch.  The deadline of each
   // checked launch is armed on the device from the best time seen so far.
   std::vector<char> launched(static_cast<size_t>(n), 0);
-  const unsigned long long best_init[4] = {0, 0, ~0ull, 0};
+  const unsigned long long best_init[5] = {0, 0, ~0ull, 0, r->empty_ns};
   LSB_CUDA(cudaMemcpyAsync(r->deadline, best_init, sizeof best_init, cudaMemcpyHostToDevice, r->st));
   LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
   const unsigned long long floor_ns = static_cast<unsigned long long>(r->opts.timeout_floor_ms * 1e6);

@@ -154,6 +154,14 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
     }
     __syncthreads();
   }
+  if (a.deadline) {  // finished past the deadline: a timeout (no timed repeats)
+    if (tid == 0) abort_flag = gtimer() > *a.deadline;
+    __syncthreads();
+    if (abort_flag) {
+      if (tid == 0) atomicExch(a.timed_out, 1);
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < RM; ++i)
 #pragma unroll
