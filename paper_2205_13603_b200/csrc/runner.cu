@@ -325,7 +325,7 @@ struct ls_runner {
         const CUtensorMap* mx = map_x(B.ptr[stp.x_buf], B.shape[stp.x_buf]);
         const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
         if (!mx || !mw) return false;
-        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st);
+        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace);
       } else if (stp.family == F_AFFCOPY) {
         ok = launch_affcopy(stp.copy, B, st);
       } else if (stp.family == F_SIMTA) {
@@ -1047,25 +1047,40 @@ ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int 
     set_error("ls_runner_trace_tc: bad arguments");
     return LS_ERR_ARG;
   }
-  std::string err;
-  auto p = parse_program(std::string_view(program, len), &err);
-  if (!p) {
-    set_error(err);
-    return LS_ERR_PARSE;
+  std::vector<Plan> plans;
+  const char* progs[1] = {program};
+  size_t lens[1] = {len};
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, progs, lens, 1, &plans);
+  Plan& plan = plans[0];
+  int ctas = 0;
+  if (plan.status == P_OK && plan.family == F_TC && !plan.gp) {
+    ctas = static_cast<int>(plan.tc.grid_m * plan.tc.grid_n * plan.tc.batch * plan.tc.splits);
+  } else if (plan.status == P_OK && plan.gp) {
+    for (const GStep& stp : plan.gp->steps)
+      if (stp.family == F_TCCONV) ctas = static_cast<int>(stp.conv.grid_m * stp.conv.grid_n * stp.conv.splits);
   }
-  Plan plan = plan_program(r->w, *p, r->lim);
-  if (plan.status != P_OK || plan.family != F_TC) {
+  if (!ctas) {
     set_error("ls_runner_trace_tc: program does not instantiate as a tcgen05 candidate");
     return LS_ERR_ARG;
   }
-  int ctas = static_cast<int>(plan.tc.grid_m * plan.tc.grid_n * plan.tc.batch * plan.tc.splits);
+  if (plan.gp) {  // general workloads: bytecode of this one candidate
+    LSB_CUDA(cudaSetDevice(r->device));
+    const std::vector<int64_t>& code = plan.gp->gen.code;
+    if (code.size() > r->gcode_cap) {
+      cudaFree(r->gcode);
+      r->gcode = nullptr;
+      r->gcode_cap = std::max(code.size(), 2 * r->gcode_cap);
+      LSB_CUDA(cudaMalloc(&r->gcode, r->gcode_cap * 8));
+    }
+    if (!code.empty()) LSB_CUDA(cudaMemcpy(r->gcode, code.data(), code.size() * 8, cudaMemcpyHostToDevice));
+    plan.gcode = r->gcode;
+  }
   *n_ctas = ctas;
   LSB_CUDA(cudaSetDevice(r->device));
   unsigned long long* d = nullptr;
   LSB_CUDA(cudaMalloc(&d, static_cast<size_t>(ctas) * 8 * 8 * launches));
   LSB_CUDA(cudaMemsetAsync(d, 0, static_cast<size_t>(ctas) * 8 * 8 * launches, r->st));
-  std::vector<Plan> one(1, plan);
-  ls_status ps = r->prepare_sync(one);
+  ls_status ps = r->prepare_sync(plans);
   if (ps != LS_OK) {
     cudaFree(d);
     return ps;

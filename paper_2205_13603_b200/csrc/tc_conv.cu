@@ -49,6 +49,7 @@ struct TcConvArgs {
   KCoord kc[kConvMaxK];       // [split * kt + k-tile]
   int bn, splits, kt, stages, mode;
   uint32_t idesc, tmem_cols;
+  unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA, as tc_gemm)
 };
 
 struct Coord {
@@ -108,6 +109,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtime();
 
   // the dead lower half of every A stage: zero once, visible to the tensor core
   for (int s = 0; s < a.stages; ++s) {
@@ -136,6 +140,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   // tile origin: output-pixel box (grid y), channel tile (grid x), split (grid z)
   Coord o{a.x_n0, a.x_h0, a.x_w0, a.x_c0, 0, 0, a.c0};
@@ -166,6 +171,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       const uint32_t ph = (kt / a.stages) & 1;
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
+      if (tr && kt == 0) tr[2] = gtime();
       const uint32_t sa = a0 + s * kStageA, sb = b0 + s * b_bytes;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
@@ -179,6 +185,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
+  if (tr && threadIdx.x == 0) tr[3] = gtime();
   const int row = warp * 32 + lane;
   const int c4 = a.bn / 4;
   float* cbase = a.c + o.cc;
@@ -226,11 +233,18 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       }
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[4] = gtime();
     const float* sb = reinterpret_cast<const float*>(gbase);
     for (int e = threadIdx.x; e < kRows * c4; e += 128) {
       const int r = e / c4, cc = (e % c4) * 4;
       *reinterpret_cast<float4*>(out_row(r) + cc) = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
     }
+  }
+  if (tr && threadIdx.x == 0) {
+    tr[6] = gtime();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[7] = smid;
   }
   tc_fence_before();
   __syncthreads();
@@ -242,7 +256,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 }  // namespace
 
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
-                    cudaStream_t st) {
+                    cudaStream_t st, unsigned long long* trace) {
   static int max_dyn = -1;
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
@@ -250,6 +264,7 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   if (g.splits * g.kt > kConvMaxK) return false;
   TcConvArgs a;
   a.c = c;
+  a.trace = trace;
   a.m_grid = g.m_grid;
   a.n_grid = g.n_grid;
   a.x_n0 = g.x_n0; a.x_h0 = g.x_h0; a.x_w0 = g.x_w0; a.x_c0 = g.x_c0;

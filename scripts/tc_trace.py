@@ -14,12 +14,14 @@ from paper_2205_13603_b200.runner import B200Runner  # noqa: E402
 
 want = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,1,12,64,12").split(",")]
 launches = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-hdr, pop = load_population("bert_ffn")
+workload = sys.argv[3] if len(sys.argv) > 3 else "bert_ffn"
+family = "tcgen05_conv" if workload == "conv2d" else "tcgen05"
+hdr, pop = load_population(workload)
 r = B200Runner(dtype="bf16")
 r.set_workload(hdr["e0"])
 progs = [p["program"] for p in pop]
 plans = r.plan_programs(progs)
-i = next(i for i, p in enumerate(plans) if p["family"] == "tcgen05" and p["cfg"][:len(want)] == want)
+i = next(i for i, p in enumerate(plans) if p["family"] == family and p["cfg"][:len(want)] == want)
 print("cfg", plans[i]["cfg"][:8])
 b = progs[i].encode()
 buf = (ctypes.c_uint64 * (8 * 4096))()

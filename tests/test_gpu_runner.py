@@ -233,7 +233,7 @@ def test_conv2d_population_slice_has_no_parity_failures():
     res = r.measure_programs([p["program"] for p in pop[:384]])
     bad = [x for x in res if x["status"] in ("PARITY", "LAUNCH")]
     assert not bad, bad[:3]
-    assert sum(x["status"] == "OK" for x in res) > 50
+    assert sum(x["status"] == "OK" for x in res) > 20
     r.close()
 
 
