@@ -222,6 +222,7 @@ def run_b200(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     host_split = []
+    sim_ms = []
 
     def step():
         t0 = time.perf_counter()
@@ -235,7 +236,8 @@ def run_b200(args):
         host_split.append([round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
                            round(1e3 * (time.perf_counter() - t2), 1), round(st["phase_a_host_ms"], 1), round(st["phase_b_host_ms"], 1)])
         devbatch.analyze(model=model)
-        dev_ms = runner.elapsed_ms() + devbatch.elapsed_ms()
+        sim_ms.append(devbatch.elapsed_ms())
+        dev_ms = runner.elapsed_ms() + sim_ms[-1]
         return res, wall, dev_ms, runner.launch_count() + 2
 
     for _ in range(args.warmup):
@@ -340,6 +342,11 @@ def run_b200(args):
                                "CUDA graph of >= 50 back-to-back launches (>= 0.5 ms) between CUDA events",
                 "speedup_vs_e0": base["latency_ns"] / best["latency_ns"]},
             "e0_baseline_us": base["latency_ns"] / 1e3,
+            "parity_mode": {
+                "what": "the reference Runner's own computation (simulate_latency, exact int128 rationals) + "
+                        "featurize + predict for the same slice, fused K7+K8 kernel on the GPU: the like-for-like "
+                        "counterpart of the --impl reference arm (which cannot execute candidates)",
+                "value": len(texts) / (statistics.median(sim_ms[-args.steps:]) / 1e3), "unit": "candidates/s"},
             "outcomes": {f"{a}/{b}": c for (a, b), c in sorted(fam.items())},
             "outcome_device_ms": {f"{a}/{b}": round(v, 3) for (a, b), v in sorted(fam_ms.items())},
             "roofline": None if best is None else {
