@@ -193,10 +193,15 @@ def run_b200(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; with fewer visible GPUs than ranks (the gloo
+    # self-test of the multi-rank path on a 1-GPU box) ranks share devices
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     hdr, pop = load_pop(args.workload)
     e0 = hdr["e0"]
@@ -263,7 +268,7 @@ def run_b200(args):
     from paper_2205_13603_b200.dist import max_over_ranks
     if world > 1:
         dist.barrier()
-    dev_ms, wall_s = max_over_ranks([sum(devs), sum(walls)], device="cuda")
+    dev_ms, wall_s = max_over_ranks([sum(devs), sum(walls)], device="cuda" if args.dist_backend == "nccl" else "cpu")
     dev_s = dev_ms / 1e3
     total_cands = len(texts) * world * args.steps
 
@@ -373,6 +378,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
     ap.add_argument("--final-top", type=int, default=8)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend for N>1 (barrier + max over ranks only); gloo lets ranks share one GPU")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--timeout-factor", type=float, default=10.0,
                     help="checked launches get clamp(factor x best-so-far, 0.05 ms, 2 x e0) before abort")

@@ -82,6 +82,7 @@ class ShardedRunner:
             self._procs.append(p)
         self._baseline = None
         self.last_device_ms = []
+        self.last_results = []
 
     def _call_all(self, cmd, payloads):
         for c, pl in zip(self._conns, payloads):
@@ -110,6 +111,7 @@ class ShardedRunner:
                 self.last_device_ms.append(v[1])
             for i, r in zip(sl, res):
                 out[i] = r
+        self.last_results = out
         return out
 
     def baseline(self, e0=None, machine_spec=None) -> Fraction:

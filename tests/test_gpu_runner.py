@@ -257,3 +257,29 @@ def test_dense_relu_general_path_exact():
         if x["status"] == "OK":
             assert x["mismatches"] == 0, x
     r.close()
+
+
+def test_sharded_runner_b200_workers_match_single_runner():
+    # the real process-per-device path (two workers sharing GPU 0 here; one
+    # per GPU on an 8-GPU box): dealt round-robin, gathered in candidate order
+    from paper_2205_13603_b200.multigpu import ShardedRunner
+    hdr, pop = load_population("bmm_qk")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop[:96]]
+    one = make_runner("bf16", timeout_ms=5.0)
+    one.set_workload(e0, seed=0)
+    want = one.measure_programs(progs)
+    one.close()
+    sh = ShardedRunner([0, 0], backend="b200", dtype="bf16", min_repeats=1, max_repeats=3, target_ms=0.005,
+                       timeout_ms=5.0)
+    try:
+        sh.set_workload(e0)
+        got = sh.measure_programs(progs)
+    finally:
+        sh.close()
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert (g["family"], g["cfg"]) == (w["family"], w["cfg"])
+        if w["status"] == "OK" and g["status"] == "OK":
+            assert g["mismatches"] == 0
+    assert sum(g["status"] == "OK" for g in got) >= 0.8 * sum(w["status"] == "OK" for w in want)
