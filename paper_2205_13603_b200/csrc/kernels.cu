@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "kernels.cuh"
 
@@ -29,6 +30,7 @@ struct SArgs {
   int lda, ldb;               // padded smem row lengths
   int a_vec_smem, b_vec_smem; // 128-bit smem reads possible
   int c_vec;                  // 128-bit output stores possible
+  int db;                     // fp32 only: cp.async double-buffered k-tiles (two smem tile sets)
   const unsigned long long* deadline;
   int* timed_out;
 };
@@ -117,6 +119,65 @@ __device__ __forceinline__ void stage_tile(float* S, int lds, const T* __restric
   }
 }
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// stage_tile for fp32 operands without a register round trip: the same index
+// walk, every element (or 16-byte run along the tile's row when rows are
+// 16-byte aligned in smem) is a cp.async, so the next k-tile streams in while
+// the current one is computed
+template <int V>
+__device__ __forceinline__ void stage_tile_async(float* S, int lds, const float* __restrict__ g, int64_t s_b,
+                                                 int64_t s_r, int64_t s_k, int64_t b0, int64_t brb, int64_t rbi,
+                                                 int64_t r0, int64_t k0, int nt, int nr, int bk, bool kfast, int tid,
+                                                 int nthr) {
+  const int nf = (kfast ? bk : nr) / V;
+  const int ns = kfast ? nr : bk;
+  const int total = nt * ns * nf;
+  if (tid >= total) return;
+  int f = tid % nf, q = tid / nf, sl = q % ns, t = q / ns;
+  const int sf = nthr % nf, sq = nthr / nf, ss = sq % ns, st = sq / ns;
+  const bool row16 = V == 4 && (lds % 4) == 0;
+  for (int e = tid; e < total; e += nthr) {
+    const int64_t b = b0 + t * brb + rbi;
+    if (kfast) {
+      const int kk = f * V, r = sl;
+      const float* src = g + b * s_b + (r0 + r) * s_r + (k0 + kk) * s_k;
+      float* d = S + (t * bk + kk) * lds + r;
+#pragma unroll
+      for (int i = 0; i < V; ++i) cp_async4(d + i * lds, src + i * s_k);
+    } else {
+      const int r = f * V, kk = sl;
+      const float* src = g + b * s_b + (r0 + r) * s_r + (k0 + kk) * s_k;
+      float* d = S + (t * bk + kk) * lds + r;
+      if (row16) {
+        cp_async16(d, src);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) cp_async4(d + i, src + i * s_r);
+      }
+    }
+    f += sf;
+    int c = 0;
+    if (f >= nf) { f -= nf; c = 1; }
+    sl += ss + c;
+    c = 0;
+    if (sl >= ns) { sl -= ns; c = 1; }
+    t += st + c;
+  }
+}
+
 template <typename T, int RM, int RN>
 __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const T* __restrict__ y,
                                                   float* __restrict__ c, SArgs a) {
@@ -130,8 +191,10 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
   const int tb_i = tid / (int)(a.tn * a.tm);
   const int bm = (int)a.tm * RM, bn = (int)a.tn * RN, bk = (int)a.bk;
   const int lda = a.lda, ldb = a.ldb;
+  const int64_t a_words = (a.tb * bk * lda + 3) & ~(int64_t)3;  // 16-byte aligned B tile
+  const int64_t set_words = (a_words + a.tb * bk * ldb + 3) & ~(int64_t)3;
   float* As = sm;
-  float* Bs = sm + ((a.tb * bk * lda + 3) & ~(int64_t)3);  // 16-byte aligned B tile
+  float* Bs = sm + a_words;
   const int64_t m0 = (int64_t)blockIdx.y * bm, n0 = (int64_t)blockIdx.x * bn;
   const int64_t b0 = (int64_t)blockIdx.z * a.tb * a.rb;
   const Strides& s = a.s;
@@ -143,28 +206,65 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
 #pragma unroll
       for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
 
+    bool async_tiles = false;
+    if constexpr (sizeof(T) == 4) async_tiles = a.db != 0;
+    auto issue_async = [&](int64_t kti, int buf) {
+      if constexpr (sizeof(T) == 4) {
+        float* A2 = sm + buf * set_words;
+        float* B2 = A2 + a_words;
+        const int64_t k0 = kti * bk;
+        if (a.va > 1)
+          stage_tile_async<VW>(A2, lda, reinterpret_cast<const float*>(x), s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi,
+                               m0, k0, (int)a.tb, bm, bk, a.x_kfast, tid, nthr);
+        else
+          stage_tile_async<1>(A2, lda, reinterpret_cast<const float*>(x), s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi,
+                              m0, k0, (int)a.tb, bm, bk, a.x_kfast, tid, nthr);
+        if (a.vb > 1)
+          stage_tile_async<VW>(B2, ldb, reinterpret_cast<const float*>(y), s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi,
+                               n0, k0, (int)a.tb, bn, bk, a.y_kfast, tid, nthr);
+        else
+          stage_tile_async<1>(B2, ldb, reinterpret_cast<const float*>(y), s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi,
+                              n0, k0, (int)a.tb, bn, bk, a.y_kfast, tid, nthr);
+      }
+      cp_async_commit();
+    };
+    if (async_tiles) issue_async(0, 0);
+
     for (int64_t kti = 0; kti < a.kt; ++kti) {
       if (a.deadline) {
         if (tid == 0) abort_flag = gtimer() > *a.deadline;
         __syncthreads();
         if (abort_flag) {
           if (tid == 0) atomicExch(a.timed_out, 1);
+          if (async_tiles) cp_async_wait<0>();
           return;
         }
       }
       const int64_t k0 = kti * bk;
-      if (a.va > 1)
-        stage_tile<T, VW>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk, a.x_kfast,
-                          tid, nthr);
-      else
-        stage_tile<T, 1>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk, a.x_kfast,
-                         tid, nthr);
-      if (a.vb > 1)
-        stage_tile<T, VW>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk, a.y_kfast,
-                          tid, nthr);
-      else
-        stage_tile<T, 1>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk, a.y_kfast,
-                         tid, nthr);
+      if (async_tiles) {
+        // tile kti was issued one iteration ago; issue kti+1 into the other set
+        if (kti + 1 < a.kt) {
+          issue_async(kti + 1, (int)((kti + 1) & 1));
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        As = sm + (kti & 1) * set_words;
+        Bs = As + a_words;
+      } else {
+        if (a.va > 1)
+          stage_tile<T, VW>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk,
+                            a.x_kfast, tid, nthr);
+        else
+          stage_tile<T, 1>(As, lda, x, s.sx[0], s.sx[1], s.sx[3], b0, a.rb, rbi, m0, k0, (int)a.tb, bm, bk,
+                           a.x_kfast, tid, nthr);
+        if (a.vb > 1)
+          stage_tile<T, VW>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk,
+                            a.y_kfast, tid, nthr);
+        else
+          stage_tile<T, 1>(Bs, ldb, y, s.sy[0], s.sy[2], s.sy[3], b0, a.rb, rbi, n0, k0, (int)a.tb, bn, bk,
+                           a.y_kfast, tid, nthr);
+      }
       __syncthreads();
       const float* Ap = As + (int64_t)tb_i * bk * lda + tm_i * RM;
       const float* Bp = Bs + (int64_t)tb_i * bk * ldb + tn_i * RN;
@@ -475,8 +575,21 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
   a.a_vec_smem = (a.lda % 4 == 0) && (cfg.rm % 4 == 0);
   a.b_vec_smem = (a.ldb % 4 == 0) && (cfg.rn % 4 == 0);
   a.c_vec = s.sc[2] == 1 && cfg.rn % 4 == 0 && s.sc[1] % 4 == 0 && s.sc[0] % 4 == 0;
-  const size_t smem = (((size_t)cfg.tb * cfg.bk * a.lda + 3) & ~(size_t)3) * sizeof(float) +
-                      (size_t)cfg.tb * cfg.bk * a.ldb * sizeof(float);
+  const size_t a_words = ((size_t)cfg.tb * cfg.bk * a.lda + 3) & ~(size_t)3;
+  size_t smem = (a_words + (size_t)cfg.tb * cfg.bk * a.ldb) * sizeof(float);
+  // fp32 with more than one k-tile: double-buffer through cp.async when two
+  // tile sets fit (the hardware validator judged the single set)
+  static int db_max = -1;
+  if (db_max < 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    db_max = v - 2048;
+  }
+  static const bool no_db = getenv("LSB_SIMT_NODB") && atoi(getenv("LSB_SIMT_NODB")) != 0;
+  const size_t set_words = (a_words + (size_t)cfg.tb * cfg.bk * a.ldb + 3) & ~(size_t)3;
+  a.db = !bf16 && !no_db && cfg.kt > 1 && 2 * set_words * sizeof(float) <= static_cast<size_t>(db_max) ? 1 : 0;
+  if (a.db) smem = 2 * set_words * sizeof(float);
   dim3 grid((unsigned)cfg.gn, (unsigned)cfg.gm, (unsigned)cfg.gb);
   return fn(x, y, c, a, grid, (int)(cfg.tb * cfg.tm * cfg.tn), smem, st) == cudaSuccess;
 }
