@@ -27,31 +27,73 @@ typedef __int128 i128;
 struct Q { i128 n, d; };
 
 __device__ __forceinline__ i128 iabs(i128 x) { return x < 0 ? -x : x; }
-__device__ i128 gcd128(i128 a, i128 b) {
-  a = iabs(a); b = iabs(b);
-  while (b) { i128 t = a % b; a = b; b = t; }
-  return a;
+__device__ __forceinline__ bool fits64(i128 x) { return x >= (i128)INT64_MIN && x <= (i128)INT64_MAX; }
+// 128-bit division is a long software routine on the GPU: take the 64-bit
+// instruction path whenever both operands fit (almost always here)
+__device__ __forceinline__ i128 qdiv(i128 a, i128 b) {
+  if (fits64(a) && fits64(b)) return (i128)((int64_t)a / (int64_t)b);
+  return a / b;
+}
+__device__ __forceinline__ int ctz128(unsigned __int128 x) {
+  const uint64_t lo = (uint64_t)x;
+  return lo ? __ffsll((long long)lo) - 1 : 64 + __ffsll((long long)(uint64_t)(x >> 64)) - 1;
+}
+// binary (Stein) gcd: shifts and subtractions only, no division
+__device__ i128 gcd128(i128 sa, i128 sb) {
+  unsigned __int128 a = (unsigned __int128)iabs(sa), b = (unsigned __int128)iabs(sb);
+  if (!a) return (i128)b;
+  if (!b) return (i128)a;
+  if (!(a >> 64) && !(b >> 64)) {
+    uint64_t x = (uint64_t)a, y = (uint64_t)b;
+    const int sh = __ffsll((long long)(x | y)) - 1;
+    x >>= __ffsll((long long)x) - 1;
+    do {
+      y >>= __ffsll((long long)y) - 1;
+      if (x > y) { uint64_t t = x; x = y; y = t; }
+      y -= x;
+    } while (y);
+    return (i128)(x << sh);
+  }
+  const int sh = ctz128(a | b);
+  a >>= ctz128(a);
+  do {
+    b >>= ctz128(b);
+    if (a > b) { unsigned __int128 t = a; a = b; b = t; }
+    b -= a;
+  } while (b);
+  return (i128)(a << sh);
 }
 __device__ Q qmk(i128 n, i128 d) {
   if (d < 0) { n = -n; d = -d; }
   i128 g = gcd128(n, d);
-  if (g > 1) { n /= g; d /= g; }
+  if (g > 1) { n = qdiv(n, g); d = qdiv(d, g); }
   return Q{n, d};
 }
 __device__ __forceinline__ Q qint(i128 x) { return Q{x, 1}; }
 constexpr i128 kQLim = ((i128)1) << 120;
+// overflow guard |x| * |y| > kQLim without a 128-bit division
+__device__ __forceinline__ bool mul_over(i128 x, i128 y) {
+  const unsigned __int128 ax = (unsigned __int128)iabs(x), ay = (unsigned __int128)iabs(y);
+  if (!ax || !ay) return false;
+  if (!(ax >> 60) && !(ay >> 60)) return false;  // < 2^120
+  return ax > (unsigned __int128)kQLim / ay;
+}
 __device__ Q qadd(Q a, Q b, int* ovf) {
+  if (a.d == 1 && b.d == 1) {  // integers: the common case
+    if (iabs(a.n) > kQLim || iabs(b.n) > kQLim) *ovf = 1;
+    return Q{a.n + b.n, 1};
+  }
   i128 g = gcd128(a.d, b.d);
-  i128 bd = b.d / g, ad = a.d / g;
-  if (iabs(a.n) > kQLim / bd || iabs(b.n) > kQLim / ad || a.d > kQLim / bd) *ovf = 1;
+  i128 bd = qdiv(b.d, g), ad = qdiv(a.d, g);
+  if (mul_over(a.n, bd) || mul_over(b.n, ad) || mul_over(a.d, bd)) *ovf = 1;
   return qmk(a.n * bd + b.n * ad, a.d * bd);
 }
 __device__ Q qmul(Q a, Q b, int* ovf) {
   i128 g1 = gcd128(a.n, b.d), g2 = gcd128(b.n, a.d);
   if (g1 == 0) g1 = 1;
   if (g2 == 0) g2 = 1;
-  i128 n1 = a.n / g1, d2 = b.d / g1, n2 = b.n / g2, d1 = a.d / g2;
-  if ((n1 && iabs(n2) > kQLim / iabs(n1)) || d1 > kQLim / d2) *ovf = 1;
+  i128 n1 = qdiv(a.n, g1), d2 = qdiv(b.d, g1), n2 = qdiv(b.n, g2), d1 = qdiv(a.d, g2);
+  if (mul_over(n1, n2) || mul_over(d1, d2)) *ovf = 1;
   return qmk(n1 * n2, d1 * d2);
 }
 
