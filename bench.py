@@ -132,6 +132,34 @@ def profiled_traffic(workload):
         return None
 
 
+def reference_search(e0_json, dtype, device, trials=64):
+    """The reference's own search (`tune`, `src/search.py:315-376`) on this
+    box's host cores next to the same search with the B200 seams installed
+    (hardware mode: every candidate executed, checked and timed on the GPU).
+    Needs the reference package (the unmodified install under baseline/_ref);
+    outside the timed region, N=1 only."""
+    try:
+        from paper_2205_13603_b200 import plugin
+        from paper_2205_13603_b200.refapi import loopsched
+        ls = loopsched()
+    except ImportError as exc:
+        return {"unavailable": str(exc)}
+    e0 = ls.ir.deserialize(e0_json)
+    cfg = ls.SearchConfig(trials=trials, batch=16, population=64, seed=0)
+    t0 = time.perf_counter()
+    ref = ls.tune(e0, ls.default_space(), cfg)
+    t_ref = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    hw = plugin.tune(e0, ls.default_space(), cfg, mode="hardware", device=device, dtype=dtype,
+                     min_repeats=3, max_repeats=50, target_ms=0.05, timeout_ms=5.0, timeout_factor=10.0)
+    t_hw = time.perf_counter() - t0
+    return {"space": "reference default space", "trials": trials, "seed": 0, "cores": 1,
+            "reference_cpu": {"wall_s": t_ref, "trials_per_s": len(ref.log) / t_ref,
+                              "best": str(ref.best_latency), "unit": "simulated cycles"},
+            "b200_hardware": {"wall_s": t_hw, "trials_per_s": len(hw.log) / t_hw,
+                              "best_ns": float(hw.best_latency), "speedup_vs_e0": hw.speedup}}
+
+
 def cpu_baseline(programs, model, budget_s=8.0):
     """The oracle port of the reference's Runner + predict on this host."""
     from oracle import oracle as O
@@ -320,6 +348,7 @@ def run_b200(args):
 
     if rank == 0:
         cpu = cpu_baseline(progs, model, budget_s=args.cpu_budget) if world == 1 else None
+        search = reference_search(e0, dtype, local) if world == 1 and args.search_trials > 0 else None
         line = {
             "metric": METRIC, "value": total_cands / dev_s, "unit": "candidates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
@@ -360,6 +389,7 @@ def run_b200(args):
                 "traffic": profiled_traffic(args.workload),
                 "kernel": f"best candidate ({best['family']}), L2-warm back-to-back repeats"},
             "cpu_baseline": cpu,
+            "reference_search": search,
         }
         print(json.dumps(line), flush=True)
     runner.close()
@@ -378,6 +408,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
     ap.add_argument("--final-top", type=int, default=8)
+    ap.add_argument("--search-trials", type=int, default=64,
+                    help="trials of the reference search timed beside ours (0 = skip)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend for N>1 (barrier + max over ranks only); gloo lets ranks share one GPU")
     ap.add_argument("--cpu-budget", type=float, default=8.0)

@@ -357,6 +357,20 @@ bool affcopy_plan(const Program& p, const Block& blk, CopyCfg* c) {
     return true;
   };
   if (!lin(s->indices, s->buffer, &c->out) || !lin(xl->kids, xl->buffer, &c->in)) return false;
+  // the kernel computes points, offsets and guard values in 32 bits
+  auto elems = [&](int buf) {
+    int64_t n = 1;
+    for (int64_t d : p.buffers[static_cast<size_t>(buf)].shape) n *= d;
+    return n;
+  };
+  if (c->points >= (1LL << 31) || elems(s->buffer) >= (1LL << 30) || elems(xl->buffer) >= (1LL << 30)) return false;
+  auto small = [](const QSum& q) {
+    if (q.c0 >= (1LL << 30) || q.c0 <= -(1LL << 30)) return false;
+    for (int i = 0; i < q.n; ++i)
+      if (q.t[i].coef >= (1LL << 30) || q.t[i].coef <= -(1LL << 30)) return false;
+    return true;
+  };
+  if (!small(c->out) || !small(c->in)) return false;
   c->in_buf = xl->buffer;
   c->out_buf = s->buffer;
   // guarded dims: with a Select guard every input dim is checked (cheap);

@@ -162,41 +162,45 @@ __global__ void generic_nest_kernel(GenBlock g, const int64_t* __restrict__ code
 }
 
 // AFFCOPY: thread per point of the block's loops (nest order, last fastest)
-__device__ __forceinline__ int64_t qsum(const QSum& q, const int64_t* lv) {
-  int64_t acc = q.c0;
+// 32-bit arithmetic throughout (every index and offset of a runner buffer
+// fits; the planner checks the buffer sizes): 64-bit division is a long
+// instruction sequence and was the kernel's bottleneck
+__device__ __forceinline__ int32_t qsum(const QSum& q, const uint32_t* lv) {
+  int32_t acc = static_cast<int32_t>(q.c0);
   for (int i = 0; i < q.n; ++i) {
     const QTerm& t = q.t[i];
-    int64_t x = lv[t.loop];
-    if (t.div > 1) x /= t.div;
-    if (t.mod) x %= t.mod;
-    acc += x * t.coef;
+    uint32_t x = lv[t.loop];
+    if (t.div > 1) x /= static_cast<uint32_t>(t.div);
+    if (t.mod) x %= static_cast<uint32_t>(t.mod);
+    acc += static_cast<int32_t>(x) * static_cast<int32_t>(t.coef);
   }
   return acc;
 }
 
 template <typename Ti, typename To>
 __global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __restrict__ in, To* __restrict__ out) {
-  for (int64_t pt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pt < c.points;
-       pt += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lv[kCopyMaxLoops];
-    int64_t rem = pt;
+  const uint32_t points = static_cast<uint32_t>(c.points);
+  for (uint32_t pt = blockIdx.x * blockDim.x + threadIdx.x; pt < points; pt += gridDim.x * blockDim.x) {
+    uint32_t lv[kCopyMaxLoops];
+    uint32_t rem = pt;
     for (int l = c.nl - 1; l >= 0; --l) {
-      const int64_t q = rem / c.ext[l];
-      lv[l] = rem - q * c.ext[l];
+      const uint32_t e = static_cast<uint32_t>(c.ext[l]);
+      const uint32_t q = rem / e;
+      lv[l] = rem - q * e;
       rem = q;
     }
     bool inb = true;
     for (int d = 0; d < c.ng; ++d) {
-      const int64_t x = qsum(c.g[d], lv);
-      inb &= x >= 0 && x < c.gext[d];
+      const int32_t x = qsum(c.g[d], lv);
+      inb &= x >= 0 && x < static_cast<int32_t>(c.gext[d]);
     }
     float v = 0.f;
     if (inb) {
-      const int64_t i = qsum(c.in, lv);
+      const int32_t i = qsum(c.in, lv);
       if constexpr (sizeof(Ti) == 2) v = __bfloat162float(in[i]);
       else v = static_cast<float>(in[i]);
     }
-    const int64_t o = qsum(c.out, lv);
+    const int32_t o = qsum(c.out, lv);
     if constexpr (sizeof(To) == 2) out[o] = __float2bfloat16_rn(v);
     else out[o] = v;
   }
