@@ -31,6 +31,10 @@ struct SArgs {
   int a_vec_smem, b_vec_smem; // 128-bit smem reads possible
   int c_vec;                  // 128-bit output stores possible
   int db;                     // fp32 only: cp.async double-buffered k-tiles (two smem tile sets)
+  int persist;                // checked launches: one wave of CTAs loops over the tiles, so a
+                              // timed-out candidate stops within one k-tile instead of draining
+                              // every remaining wave of its grid
+  int64_t ntn, ntm, ntb;      // tile counts (grid x, y, z of the plain launch)
   const unsigned long long* deadline;
   int* timed_out;
 };
@@ -195,9 +199,18 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
   const int64_t set_words = (a_words + a.tb * bk * ldb + 3) & ~(int64_t)3;
   float* As = sm;
   float* Bs = sm + a_words;
-  const int64_t m0 = (int64_t)blockIdx.y * bm, n0 = (int64_t)blockIdx.x * bn;
-  const int64_t b0 = (int64_t)blockIdx.z * a.tb * a.rb;
   const Strides& s = a.s;
+  const int64_t ntiles = a.persist ? a.ntn * a.ntm * a.ntb : 1;
+  for (int64_t tile = a.persist ? blockIdx.x : 0; tile < ntiles; tile += a.persist ? gridDim.x : 1) {
+  int64_t bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  if (a.persist) {
+    bx = tile % a.ntn;
+    by = (tile / a.ntn) % a.ntm;
+    bz = tile / (a.ntn * a.ntm);
+    __syncthreads();  // the previous tile's last smem reads are done
+  }
+  const int64_t m0 = by * bm, n0 = bx * bn;
+  const int64_t b0 = bz * a.tb * a.rb;
 
   for (int64_t rbi = 0; rbi < a.rb; ++rbi) {
     float acc[RM][RN];
@@ -332,6 +345,7 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
       for (int j = 0; j < RN; ++j) crow[i * s.sc[1] + j * s.sc[2]] = acc[i][j];
     }
   }
+  }  // tile loop
 }
 
 // ---- LOOPNEST family ---------------------------------------------------------
@@ -457,7 +471,33 @@ cudaError_t simt_launch(const void* x, const void* y, float* c, const SArgs& a, 
     if (max_dyn <= 0) return cudaErrorInvalidValue;
   }
   if (smem > static_cast<size_t>(max_dyn)) return cudaErrorInvalidValue;
-  fn<<<grid, threads, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(y), c, a);
+  if (a.persist) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    const int64_t tiles = static_cast<int64_t>(grid.x) * grid.y * grid.z;
+    const int64_t wave = static_cast<int64_t>(sms) * per_sm;
+    if (tiles > wave) {
+      SArgs p = a;
+      p.ntn = grid.x;
+      p.ntm = grid.y;
+      p.ntb = grid.z;
+      fn<<<dim3(static_cast<unsigned>(wave)), threads, smem, st>>>(static_cast<const T*>(x),
+                                                                   static_cast<const T*>(y), c, p);
+      return cudaGetLastError();
+    }
+  }
+  SArgs p = a;
+  p.persist = 0;
+  fn<<<grid, threads, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(y), c, p);
   return cudaGetLastError();
 }
 
@@ -557,6 +597,9 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
   a.tb = cfg.tb; a.tm = cfg.tm; a.tn = cfg.tn; a.rb = cfg.rb; a.bk = cfg.bk; a.kt = cfg.kt;
   a.deadline = deadline;
   a.timed_out = timed_out;
+  static const bool no_persist = getenv("LSB_SIMT_NOPERSIST") && atoi(getenv("LSB_SIMT_NOPERSIST")) != 0;
+  a.persist = deadline && !no_persist ? 1 : 0;
+  a.ntn = a.ntm = a.ntb = 1;
   const int64_t bm = cfg.tm * cfg.rm, bn = cfg.tn * cfg.rn;
   const int vw = bf16 ? 8 : 4;
   // operand X (rows = M): contiguous along k or m?

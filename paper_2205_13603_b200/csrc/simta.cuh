@@ -23,6 +23,8 @@ struct SimtaArgs {
   int64_t gm, gn, tm, tn, bk, kt;
   const unsigned long long* deadline;
   int* timed_out;
+  int persist;              // checked launches: one wave loops over the tiles (fast timeouts, see kernels.cu)
+  int64_t ntn, ntm;         // tile counts of the plain grid (x, y)
 };
 
 int opt_in_dynamic_smem(const void* fn);

@@ -81,9 +81,11 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
     decode(a.k_bk, kk, &sx, &sy, &sc, &g0, &g1);
     offXK[kk] = (int)sx; offYK[kk] = (int)sy; gK0[kk] = (int)g0; gK1[kk] = (int)g1;
   }
+  const int64_t ntiles = a.persist ? a.ntn * a.ntm : 1;
+  for (int64_t tile = a.persist ? blockIdx.x : 0; tile < ntiles; tile += a.persist ? gridDim.x : 1) {
   int64_t bx = a.x0, by = a.y0, bc = a.c0, bg0 = a.g0[0], bg1 = a.g0[1];
-  decode(a.m_grid, blockIdx.y, &bx, &by, &bc, &bg0, &bg1);
-  decode(a.n_grid, blockIdx.x, &bx, &by, &bc, &bg0, &bg1);
+  decode(a.m_grid, a.persist ? tile / a.ntn : blockIdx.y, &bx, &by, &bc, &bg0, &bg1);
+  decode(a.n_grid, a.persist ? tile % a.ntn : blockIdx.x, &bx, &by, &bc, &bg0, &bg1);
   __syncthreads();
 
   float acc[RM][RN];
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
   for (int i = 0; i < RM; ++i)
 #pragma unroll
     for (int j = 0; j < RN; ++j) c[bc + offCM[tm_i * RM + i] + offCN[tn_i * RN + j]] = acc[i][j];
+  }  // tile loop
 }
 
 template <typename T, int RM, int RN>
@@ -177,8 +180,33 @@ cudaError_t launch_one(const void* x, const void* y, float* c, const SimtaArgs& 
     if (max_dyn <= 0) return cudaErrorInvalidValue;
   }
   if (smem > static_cast<size_t>(max_dyn)) return cudaErrorInvalidValue;
+  const int threads = static_cast<int>(a.tm * a.tn);
+  if (a.persist) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    const int64_t wave = static_cast<int64_t>(sms) * per_sm;
+    if (a.gn * a.gm > wave) {
+      SimtaArgs p = a;
+      p.ntn = a.gn;
+      p.ntm = a.gm;
+      fn<<<dim3(static_cast<unsigned>(wave)), threads, smem, st>>>(static_cast<const T*>(x),
+                                                                   static_cast<const T*>(y), c, p);
+      return cudaGetLastError();
+    }
+  }
+  SimtaArgs p = a;
+  p.persist = 0;
   dim3 grid(static_cast<unsigned>(a.gn), static_cast<unsigned>(a.gm), 1);
-  fn<<<grid, static_cast<unsigned>(a.tm * a.tn), smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(y), c, a);
+  fn<<<grid, threads, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(y), c, p);
   return cudaGetLastError();
 }
 
