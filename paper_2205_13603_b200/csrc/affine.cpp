@@ -386,6 +386,37 @@ bool affcopy_plan(const Program& p, const Block& blk, CopyCfg* c) {
       ++c->ng;
     }
   }
+  // contiguous innermost run: loop l joins when its only term in both the
+  // input and the output offsets is a plain `coef * v_l` with coef == run so
+  // far, and no guard looks at it
+  {
+    auto only_plain = [](const QSum& q, int l, int64_t want) {
+      int found = 0;
+      for (int i = 0; i < q.n; ++i)
+        if (q.t[i].loop == l) {
+          if (q.t[i].div != 1 || q.t[i].mod != 0 || q.t[i].coef != want) return false;
+          ++found;
+        }
+      return found == 1;
+    };
+    auto absent = [](const QSum& q, int l) {
+      for (int i = 0; i < q.n; ++i)
+        if (q.t[i].loop == l) return false;
+      return true;
+    };
+    c->run_loops = 0;
+    c->run = 1;
+    for (int l = c->nl - 1; l >= 0; --l) {
+      bool ok = only_plain(c->in, l, c->run) && only_plain(c->out, l, c->run);
+      for (int d = 0; d < c->ng && ok; ++d) ok = absent(c->g[d], l);
+      if (!ok) break;
+      c->run *= c->ext[l];
+      ++c->run_loops;
+    }
+    c->vec = 1;
+    for (int v : {8, 4, 2})
+      if (c->run % v == 0) { c->vec = v; break; }
+  }
   // host check on corners + 256 samples: the guard is exactly the load's
   // in-bounds predicate, and an unguarded load never leaves its buffer
   std::mt19937_64 rng(777);

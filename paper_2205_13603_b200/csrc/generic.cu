@@ -179,11 +179,23 @@ __device__ __forceinline__ int32_t qsum(const QSum& q, const uint32_t* lv) {
 
 template <typename Ti, typename To>
 __global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __restrict__ in, To* __restrict__ out) {
-  const uint32_t points = static_cast<uint32_t>(c.points);
-  for (uint32_t pt = blockIdx.x * blockDim.x + threadIdx.x; pt < points; pt += gridDim.x * blockDim.x) {
+  // thread unit: `vec` consecutive elements of the contiguous innermost run
+  const uint32_t vec = static_cast<uint32_t>(c.vec);
+  const uint32_t units = static_cast<uint32_t>(c.points / c.vec);
+  const int outer = c.nl - c.run_loops;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += gridDim.x * blockDim.x) {
     uint32_t lv[kCopyMaxLoops];
-    uint32_t rem = pt;
-    for (int l = c.nl - 1; l >= 0; --l) {
+    // digits of the run loops come from the element index inside the run
+    const uint32_t per_run = static_cast<uint32_t>(c.run) / vec;
+    uint32_t rem = u / per_run;
+    uint32_t e0 = (u - rem * per_run) * vec;
+    for (int l = c.nl - 1; l >= outer; --l) {
+      const uint32_t e = static_cast<uint32_t>(c.ext[l]);
+      const uint32_t q = e0 / e;
+      lv[l] = e0 - q * e;
+      e0 = q;
+    }
+    for (int l = outer - 1; l >= 0; --l) {
       const uint32_t e = static_cast<uint32_t>(c.ext[l]);
       const uint32_t q = rem / e;
       lv[l] = rem - q * e;
@@ -194,15 +206,16 @@ __global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __re
       const int32_t x = qsum(c.g[d], lv);
       inb &= x >= 0 && x < static_cast<int32_t>(c.gext[d]);
     }
-    float v = 0.f;
-    if (inb) {
-      const int32_t i = qsum(c.in, lv);
-      if constexpr (sizeof(Ti) == 2) v = __bfloat162float(in[i]);
-      else v = static_cast<float>(in[i]);
+    const int32_t i0 = qsum(c.in, lv), o0 = qsum(c.out, lv);
+    for (uint32_t k = 0; k < vec; ++k) {
+      float v = 0.f;
+      if (inb) {
+        if constexpr (sizeof(Ti) == 2) v = __bfloat162float(in[i0 + k]);
+        else v = static_cast<float>(in[i0 + k]);
+      }
+      if constexpr (sizeof(To) == 2) out[o0 + k] = __float2bfloat16_rn(v);
+      else out[o0 + k] = v;
     }
-    const int32_t o = qsum(c.out, lv);
-    if constexpr (sizeof(To) == 2) out[o] = __float2bfloat16_rn(v);
-    else out[o] = v;
   }
 }
 
@@ -212,7 +225,7 @@ bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st) {
   const int ti = B.dtype[c.in_buf], to = B.dtype[c.out_buf];
   if (ti > 1 || to > 1) return false;
   const int threads = 256;
-  int64_t blocks = (c.points + threads - 1) / threads;
+  int64_t blocks = (c.points / c.vec + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   const void* in = B.ptr[c.in_buf];

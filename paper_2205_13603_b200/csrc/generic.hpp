@@ -74,6 +74,11 @@ struct CopyCfg {
   QSum g[kCopyMaxGuard];        // guarded input dims (index values)
   int64_t gext[kCopyMaxGuard] = {0};
   int64_t points = 1;
+  // innermost loops that walk both buffers contiguously (coef 1, run, ...)
+  // and no guard: one thread copies `vec` consecutive elements of that run
+  int run_loops = 0;        // how many innermost loops form the run
+  int64_t run = 1;          // elements per run
+  int vec = 1;              // elements per thread (divides run)
 };
 
 }  // namespace lsb

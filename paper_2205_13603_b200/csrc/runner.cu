@@ -255,9 +255,17 @@ struct ls_runner {
     size_t words = 0;
     for (size_t i = 0; i < plans.size(); ++i) {
       const Plan& p = plans[i];
-      if (p.status != P_OK || p.family != F_TC || p.gp) continue;
-      if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n, p.tc.grid_n).mode != 2)
-        continue;
+      if (p.status != P_OK) continue;
+      if (p.gp) {  // tcgen05 conv step with split-K: mode 2 in tc_conv.cu
+        bool want = false;
+        for (const GStep& stp : p.gp->steps)
+          want |= stp.family == F_TCCONV && stp.conv.splits > 1 && stp.conv.grid_m * stp.conv.grid_n <= kTcSyncSlots;
+        if (!want) continue;
+      } else {
+        if (p.family != F_TC) continue;
+        if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n, p.tc.grid_n).mode != 2)
+          continue;
+      }
       sync_off[i] = static_cast<int64_t>(words);
       words += 2 * kTcSyncSlots;
     }
@@ -314,7 +322,7 @@ struct ls_runner {
     return true;
   }
 
-  bool launch_general(const Plan& p, const unsigned long long* dl, int* flag) {
+  bool launch_general(const Plan& p, const unsigned long long* dl, int* flag, int slot) {
     GenBuffers B;
     if (!general_buffers(p, &B)) return false;
     for (const GStep& stp : p.gp->steps) {
@@ -325,7 +333,10 @@ struct ls_runner {
         const CUtensorMap* mx = map_x(B.ptr[stp.x_buf], B.shape[stp.x_buf]);
         const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
         if (!mx || !mw) return false;
-        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace);
+        uint32_t* sy = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
+                           ? tcsync + sync_off[static_cast<size_t>(slot)]
+                           : nullptr;
+        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace, sy);
       } else if (stp.family == F_AFFCOPY) {
         ok = launch_affcopy(stp.copy, B, st);
       } else if (stp.family == F_SIMTA) {
@@ -355,7 +366,7 @@ struct ls_runner {
     int* flag = flags + slot;
     if (p.gp) {
       launches += static_cast<int64_t>(p.gp->steps.size());
-      return launch_general(p, dl, flag);
+      return launch_general(p, dl, flag, slot);
     }
     const size_t cbytes = static_cast<size_t>(w.c_elems) * sizeof(float);
     if (p.needs_zero && cudaMemsetAsync(c, 0, cbytes, st) != cudaSuccess) return false;

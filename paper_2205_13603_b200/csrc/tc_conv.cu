@@ -5,8 +5,9 @@
 // the upper 64 rows of a 128-row, 128-byte-swizzled operand stage -- the
 // zero padding of the convolution is TMA's out-of-bounds fill, so an inlined
 // pad stage costs nothing -- and the matching [BN x 64] slice of the K-major
-// weight copy.  The lower 64 rows stay zero, so the UMMA tile is 128 x BN
-// with half its rows live (M = 64 output pixels per box).
+// weight copy.  The lower 64 rows are dead (never written, never read back):
+// the UMMA tile is 128 x BN with half its rows live (M = 64 output pixels
+// per box).
 //
 // Warp roles and pipeline as in tc_gemm.cu (TMA producer lane, single MMA
 // issuer, S-stage mbarrier ring, PDL).  Filter-row parts hoisted above every
@@ -50,6 +51,7 @@ struct TcConvArgs {
   int bn, splits, kt, stages, mode;
   uint32_t idesc, tmem_cols;
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA, as tc_gemm)
+  uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets + [kTcSyncSlots] zeroing flags per tile
 };
 
 struct Coord {
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(128, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                const __grid_constant__ TcConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -113,12 +116,10 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = gtime();
 
-  // the dead lower half of every A stage: zero once, visible to the tensor core
-  for (int s = 0; s < a.stages; ++s) {
-    uint4* z = reinterpret_cast<uint4*>(gbase + s * kStageA + kLiveA);
-    for (int i = threadIdx.x; i < kLiveA / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  // The dead lower half of every A stage (rows 64..127) is left as it is:
+  // row r of the accumulator depends on A row r only, and rows 64..127 are
+  // never read back, so whatever the smem holds there cannot reach C
+  // (zeroing it cost ~0.5 us of every CTA's setup).
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -150,6 +151,28 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+  float* cbase = a.c + o.cc;
+  auto out_row = [&](int r) { return cbase + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1; };
+  const int c4 = a.bn / 4;
+  if (a.mode == 2 && warp >= 2) {
+    // split-K through L2 (as tc_gemm.cu mode 2): arrival ticket per tile; the
+    // first CTA of the tile to start zeroes its 64 x BN output box while its
+    // operands stream in and releases this launch's epoch
+    const int t2 = threadIdx.x - 64;
+    if (t2 == 0) s_ticket = atomicAdd(a.sync + tile, 1u);
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const uint32_t t = s_ticket;
+    if (t % static_cast<uint32_t>(a.splits) == 0) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int e = t2; e < kRows * c4; e += 64) {
+        const int r = e / c4, cc = (e % c4) * 4;
+        *reinterpret_cast<float4*>(out_row(r) + cc) = z;
+      }
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      if (t2 == 0) st_release_u32(a.sync + kTcSyncSlots + tile, t / static_cast<uint32_t>(a.splits) + 1);
+    }
+  }
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -187,9 +210,6 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   tc_fence_after();
   if (tr && threadIdx.x == 0) tr[3] = gtime();
   const int row = warp * 32 + lane;
-  const int c4 = a.bn / 4;
-  float* cbase = a.c + o.cc;
-  auto out_row = [&](int r) { return cbase + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1; };
   if (a.mode == 1) {
     const uint32_t me = cluster_rank();
     if (warp < 2) {
@@ -234,10 +254,19 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[4] = gtime();
+    if (a.mode == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
+      if (threadIdx.x == 0)
+        while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
+        }
+      __syncthreads();
+    }
+    if (tr && threadIdx.x == 0) tr[5] = gtime();
     const float* sb = reinterpret_cast<const float*>(gbase);
     for (int e = threadIdx.x; e < kRows * c4; e += 128) {
       const int r = e / c4, cc = (e % c4) * 4;
-      *reinterpret_cast<float4*>(out_row(r) + cc) = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
+      const float4 v = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
+      if (a.mode == 2) red_add_f4(out_row(r) + cc, v);
+      else *reinterpret_cast<float4*>(out_row(r) + cc) = v;
     }
   }
   if (tr && threadIdx.x == 0) {
@@ -256,7 +285,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 }  // namespace
 
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
-                    cudaStream_t st, unsigned long long* trace) {
+                    cudaStream_t st, unsigned long long* trace, uint32_t* sync) {
   static int max_dyn = -1;
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
@@ -286,7 +315,10 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   a.splits = static_cast<int>(g.splits);
   a.kt = static_cast<int>(g.kt);
   a.stages = static_cast<int>(g.stages);
-  a.mode = g.splits == 1 ? 0 : 1;
+  // split-K: L2 reduction with arrival tickets (mode 2) when the runner gave
+  // ticket slots; the cluster DSMEM reduction (mode 1) otherwise
+  a.mode = g.splits == 1 ? 0 : (sync && g.grid_m * g.grid_n <= kTcSyncSlots ? 2 : 1);
+  a.sync = sync;
   a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(g.bn >> 3) << 17) |
             (static_cast<uint32_t>(128 >> 4) << 24);
   uint32_t cols = 32;
@@ -309,7 +341,7 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = a.mode == 1 ? static_cast<unsigned>(g.splits) : 1u;
+  attr[0].val.clusterDim.z = a.mode == 1 ? static_cast<unsigned>(g.splits) : 1u;  // mode 2: no cluster
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
