@@ -203,6 +203,9 @@ def run_reference(args):
             "config": {"workload": args.workload, "candidates_per_step": len(texts),
                        "path": "reference Runner simulate_latency + featurize + predict_features "
                                "(C oracle port of src/machine.py:228-254, src/costmodel.py:21-102)"},
+            "note": "the reference Runner computes an analytic cost (simulate_latency) and executes no "
+                    "candidate; the same computation on the GPU is the b200 arm's parity_mode.value, while the "
+                    "b200 arm's value/e2e execute, check and time every candidate on the hardware",
             "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": threads, "kind": "port",
                              "sample": f"{len(texts)} programs x {args.steps} steps"},
             "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0,

@@ -84,6 +84,22 @@ bool make_c_map(CUtensorMap* map, void* base, int64_t batch, int64_t m, int64_t 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 NHWC output [n][p][q][k] as a 4-D TMA map with a {32, 8, 8, 1} box and
+// the 128-byte swizzle (the tcgen05 conv epilogue's staged chunk layout).
+bool make_nhwc_out_map(CUtensorMap* map, void* base, const int64_t* shape) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || shape[3] % 4 != 0) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(shape[3]), static_cast<cuuint64_t>(shape[2]),
+                        static_cast<cuuint64_t>(shape[1]), static_cast<cuuint64_t>(shape[0])};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(shape[3] * 4), static_cast<cuuint64_t>(shape[2] * shape[3] * 4),
+                           static_cast<cuuint64_t>(shape[1] * shape[2] * shape[3] * 4)};
+  cuuint32_t box[4] = {32, 8, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // bf16 NHWC activation [n][h][w][c] as a 4-D TMA map with an {64, 8, 8, 1}
 // box (one 8 x 8 pixel box x 64 channels); out-of-bounds boxes read zeros.
 bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape) {
@@ -183,6 +199,7 @@ struct ls_runner {
     wt = nullptr;
     tmap_wt.clear();
     tmap_x.clear();
+    tmap_o.clear();
     gbuf_dtype.clear();
     general = false;
     pfree(x); pfree(y); pfree(yk); pfree(c); pfree(ref);
@@ -299,6 +316,14 @@ struct ls_runner {
     if (!wt || !make_kmajor_map(&m, wt, 1, wt_cols, wt_rows, bn)) return nullptr;
     return &(tmap_wt[bn] = m);
   }
+  std::map<const void*, CUtensorMap> tmap_o;  // fp32 NHWC conv outputs, box {32, 8, 8, 1}
+  const CUtensorMap* map_o(const void* buf, const int64_t* shape) {
+    auto it = tmap_o.find(buf);
+    if (it != tmap_o.end()) return &it->second;
+    CUtensorMap m;
+    if (!make_nhwc_out_map(&m, const_cast<void*>(buf), shape)) return nullptr;
+    return &(tmap_o[buf] = m);
+  }
   const CUtensorMap* map_x(const void* buf, const int64_t* shape) {
     auto it = tmap_x.find(buf);
     if (it != tmap_x.end()) return &it->second;
@@ -336,7 +361,11 @@ struct ls_runner {
         uint32_t* sy = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
                            ? tcsync + sync_off[static_cast<size_t>(slot)]
                            : nullptr;
-        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace, sy);
+        const CUtensorMap* mc = p.gp->gen.ndim[stp.c_buf] == 4 && B.dtype[stp.c_buf] == 1
+                                    ? map_o(B.ptr[stp.c_buf], B.shape[stp.c_buf])
+                                    : nullptr;
+        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace, sy, mc,
+                            mc ? B.shape[stp.c_buf] : nullptr);
       } else if (stp.family == F_AFFCOPY) {
         ok = launch_affcopy(stp.copy, B, st);
       } else if (stp.family == F_SIMTA) {

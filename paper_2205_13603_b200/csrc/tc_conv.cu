@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -52,6 +53,8 @@ struct TcConvArgs {
   uint32_t idesc, tmem_cols;
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA, as tc_gemm)
   uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets + [kTcSyncSlots] zeroing flags per tile
+  int tma_epi;                // modes 0/2: 128B-swizzled [64 px][32 ch] chunks -> 4-D TMA store / add-reduce
+  int64_t oshape[4];          // output [n][p][q][k] (decodes the box origin for the C tensor map)
 };
 
 struct Coord {
@@ -91,7 +94,7 @@ void host_add_parts(const CList& L, int64_t idx, Coord& a) {
 
 __global__ void __launch_bounds__(128, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
-               const __grid_constant__ TcConvArgs a) {
+               const __grid_constant__ CUtensorMap tmc, const __grid_constant__ TcConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
@@ -240,6 +243,51 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         }
       *reinterpret_cast<float4*>(out_row(r_lo + lr2) + cc) = acc;
     }
+  } else if (a.tma_epi) {
+    // TMEM rows 0..63 -> [64 px][32 ch] fp32 chunks, 128-byte swizzle (unit q of
+    // row r at q ^ (r & 7)), then one 4-D TMA store / add-reduce per chunk
+    if (warp < 2) {
+      const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+      for (int c0 = 0; c0 < a.bn; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld16_nowait(trow + c0, v);
+        tmem_ld16_nowait(trow + c0 + 16, v + 16);
+        tmem_wait();
+        uint8_t* chunk = gbase + (c0 / 32) * 8192 + row * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(chunk + ((q ^ (row & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                          __uint_as_float(v[4 * q + 3]));
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tr && threadIdx.x == 0) tr[4] = gtime();
+    if (a.mode == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
+      if (threadIdx.x == 0)
+        while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
+        }
+      __syncthreads();
+    }
+    if (tr && threadIdx.x == 0) tr[5] = gtime();
+    if (threadIdx.x == 0) {
+      int64_t off = o.cc;
+      const int co0 = static_cast<int>(off % a.oshape[3]);
+      off /= a.oshape[3];
+      const int q0 = static_cast<int>(off % a.oshape[2]);
+      off /= a.oshape[2];
+      const int p0 = static_cast<int>(off % a.oshape[1]);
+      const int n0 = static_cast<int>(off / a.oshape[1]);
+      fence_proxy_async_global();
+      for (int c0 = 0; c0 < a.bn; c0 += 32) {
+        const uint32_t src = base + (c0 / 32) * 8192;
+        if (a.mode == 2) tma_reduce_add_4d(&tmc, src, co0 + c0, q0, p0, n0);
+        else tma_store_4d(&tmc, src, co0 + c0, q0, p0, n0);
+      }
+      bulk_commit();
+      bulk_wait_all();
+    }
   } else {
     if (warp < 2) {
       float* stg = reinterpret_cast<float*>(gbase) + row * red_ld;
@@ -285,7 +333,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 }  // namespace
 
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
-                    cudaStream_t st, unsigned long long* trace, uint32_t* sync) {
+                    cudaStream_t st, unsigned long long* trace, uint32_t* sync, const void* tmap_c,
+                    const int64_t* oshape) {
   static int max_dyn = -1;
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
@@ -319,6 +368,15 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   // ticket slots; the cluster DSMEM reduction (mode 1) otherwise
   a.mode = g.splits == 1 ? 0 : (sync && g.grid_m * g.grid_n <= kTcSyncSlots ? 2 : 1);
   a.sync = sync;
+  // TMA epilogue: the 64 box rows are the 8 x 8 pixels of an NHWC output
+  // ([n][p][q][k], row r -> (p0 + r/8, q0 + r%8)) and BN is whole 32-ch chunks
+  static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
+  a.tma_epi = 0;
+  if (tmap_c && oshape && !no_tma_epi && a.mode != 1 && g.bn % 32 == 0 && g.cc_w1 == oshape[3] &&
+      g.cc_h1 == oshape[2] * oshape[3]) {
+    a.tma_epi = 1;
+    for (int d = 0; d < 4; ++d) a.oshape[d] = oshape[d];
+  }
   a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(g.bn >> 3) << 17) |
             (static_cast<uint32_t>(128 >> 4) << 24);
   uint32_t cols = 32;
@@ -348,7 +406,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   cfg.numAttrs = 2;
   const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
   const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
-  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, a) != cudaSuccess) {
+  const CUtensorMap tcm = a.tma_epi ? *static_cast<const CUtensorMap*>(tmap_c) : tw;
+  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, tcm, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }

@@ -10,6 +10,7 @@ namespace lsb {
 // tmap_x: 4-D bf16 map over the X-side buffer [n][h][w][c], box {64, 8, 8, 1};
 // tmap_w: 3-D bf16 map over the K-major weight copy [co][k_flat], box {64, bn, 1}.
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& cfg, bool pdl,
-                    cudaStream_t st, unsigned long long* trace = nullptr, uint32_t* sync = nullptr);
+                    cudaStream_t st, unsigned long long* trace = nullptr, uint32_t* sync = nullptr,
+                    const void* tmap_c = nullptr, const int64_t* oshape = nullptr);
 
 }  // namespace lsb
