@@ -252,7 +252,7 @@ def run_b200(args):
     timeout_ms = max(0.05, 2.0 * base["latency_ns"] / 1e6)
     runner = B200Runner(device=local, dtype=dtype, min_repeats=3, max_repeats=50, target_ms=0.02,
                         timeout_ms=timeout_ms, timeout_factor=args.timeout_factor,
-                        timeout_floor_ms=0.05)
+                        timeout_floor_ms=0.05, single_shot_factor=args.single_shot_factor)
     scorer = GpuScorer(local)
     devbatch = DeviceBatch(texts, device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -362,7 +362,8 @@ def run_b200(args):
                        "l2": "flushed (256 MB scrub) between steps; candidate repeats run L2-warm",
                        "runner": {"min_repeats": 3, "max_repeats": 50, "target_ms": 0.02,
                                   "timeout_cap_ms": round(timeout_ms, 4), "timeout_factor": args.timeout_factor,
-                                  "timeout_floor_ms": 0.05, "parity": "exact (integer inputs)"}},
+                                  "timeout_floor_ms": 0.05, "single_shot_factor": args.single_shot_factor,
+                                  "parity": "exact (integer inputs)"}},
             "e2e": {"value": total_cands / wall_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "step_ms": [round(1e3 * w, 2) for w in walls]},
             "device_step_ms": [round(d, 2) for d in devs],
@@ -411,6 +412,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert_ffn")
     ap.add_argument("--per-rank", type=int, default=1024)
     ap.add_argument("--final-top", type=int, default=8)
+    ap.add_argument("--single-shot-factor", type=float, default=5.0,
+                    help="candidates slower than this x the step's fastest checked launch skip timed repeats")
     ap.add_argument("--search-trials", type=int, default=64,
                     help="trials of the reference search timed beside ours (0 = skip)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",

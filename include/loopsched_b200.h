@@ -96,6 +96,10 @@ typedef struct {
   int32_t reserved0;
   double timeout_factor;   /* >0: deadline = clamp(factor x best-so-far, floor,   */
   double timeout_floor_ms; /*      timeout_ms), tracked on the device              */
+  double single_shot_factor; /* >0: a candidate whose checked launch is slower than */
+                           /* factor x the batch's fastest checked launch skips the */
+                           /* timed repeats; its latency is the checked launch      */
+                           /* (repeats = 0)                                         */
 } ls_runner_opts;
 
 /* per-candidate status */

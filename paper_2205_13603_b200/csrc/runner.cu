@@ -662,6 +662,7 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   o.atol = 0.0;
   o.timeout_factor = 0.0;
   o.timeout_floor_ms = 0.05;
+  o.single_shot_factor = 0.0;
   if (opts) o = *opts;
   if (o.min_repeats < 1) o.min_repeats = 1;
   if (o.max_repeats < o.min_repeats) o.max_repeats = o.min_repeats;
@@ -947,6 +948,24 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   // If capture fails the repeats are launched directly behind a device spin
   // sized to the host enqueue time.
   std::vector<int> reps(static_cast<size_t>(n), 0);
+  // slow candidates (checked launch > single_shot_factor x the fastest one)
+  // are not worth timed repeats: they report their checked launch
+  std::vector<char> single(static_cast<size_t>(n), 0);
+  if (r->opts.single_shot_factor > 0.0) {
+    float best_warm = 0.f;
+    for (int i = 0; i < n; ++i)
+      if (launched[static_cast<size_t>(i)] && out[i].status == LS_RUN_OK &&
+          (best_warm == 0.f || warm[static_cast<size_t>(i)] < best_warm))
+        best_warm = warm[static_cast<size_t>(i)];
+    for (int i = 0; i < n; ++i)
+      if (launched[static_cast<size_t>(i)] && best_warm > 0.f &&
+          warm[static_cast<size_t>(i)] > r->opts.single_shot_factor * best_warm) {
+        single[static_cast<size_t>(i)] = 1;
+        launched[static_cast<size_t>(i)] = 0;
+        out[i].repeats = 0;
+        out[i].latency_ns = 1e6 * static_cast<double>(warm[static_cast<size_t>(i)]);
+      }
+  }
   std::vector<cudaGraphExec_t> execs;
   const int chunk = 32;
   double prev_gpu_us = 0.0;

@@ -43,7 +43,7 @@ class RunnerOptsC(ctypes.Structure):
                 ("timeout_ms", ctypes.c_double), ("rtol", ctypes.c_double),
                 ("atol", ctypes.c_double), ("flush_l2", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("timeout_factor", ctypes.c_double),
-                ("timeout_floor_ms", ctypes.c_double)]
+                ("timeout_floor_ms", ctypes.c_double), ("single_shot_factor", ctypes.c_double)]
 
 
 class ResultC(ctypes.Structure):

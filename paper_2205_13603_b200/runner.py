@@ -44,7 +44,8 @@ class B200Runner:
     def __init__(self, device: int = 0, dtype: str = "bf16", min_repeats: int = 3,
                  max_repeats: int = 200, target_ms: float = 0.2, timeout_ms: float = 2.0,
                  rtol: float = 0.0, atol: float = 0.0, sentinel_factor: float = 1e4,
-                 timeout_factor: float = 0.0, timeout_floor_ms: float = 0.05):
+                 timeout_factor: float = 0.0, timeout_floor_ms: float = 0.05,
+                 single_shot_factor: float = 0.0):
         L = native.lib()
         o = native.RunnerOptsC()
         o.dtype = 1 if dtype == "bf16" else 0
@@ -52,6 +53,7 @@ class B200Runner:
         o.target_ms, o.timeout_ms = target_ms, timeout_ms
         o.rtol, o.atol = rtol, atol
         o.timeout_factor, o.timeout_floor_ms = timeout_factor, timeout_floor_ms
+        o.single_shot_factor = single_shot_factor
         h = ctypes.c_void_p()
         native.check(L.ls_runner_create(device, ctypes.byref(o), ctypes.byref(h)),
                      "ls_runner_create")

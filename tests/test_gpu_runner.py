@@ -283,3 +283,19 @@ def test_sharded_runner_b200_workers_match_single_runner():
         if w["status"] == "OK" and g["status"] == "OK":
             assert g["mismatches"] == 0
     assert sum(g["status"] == "OK" for g in got) >= 0.8 * sum(w["status"] == "OK" for w in want)
+
+
+def test_single_shot_factor_skips_repeats_of_slow_candidates():
+    hdr, pop = load_population("bmm_qk")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop[:128]]
+    r = make_runner("bf16", timeout_ms=5.0, min_repeats=3, max_repeats=3, single_shot_factor=4.0)
+    r.set_workload(e0, seed=0)
+    res = r.measure_programs(progs)
+    ok = [x for x in res if x["status"] == "OK"]
+    best = min(x["latency_ns"] for x in ok)
+    singles = [x for x in ok if x["repeats"] == 0]
+    assert singles and all(x["mismatches"] == 0 for x in ok)
+    assert all(x["latency_ns"] > 2.0 * best for x in singles)
+    assert all(x["repeats"] == 3 for x in ok if x["latency_ns"] < 2.0 * best)
+    r.close()
