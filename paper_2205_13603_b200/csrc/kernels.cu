@@ -281,8 +281,14 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
       __syncthreads();
       const float* Ap = As + (int64_t)tb_i * bk * lda + tm_i * RM;
       const float* Bp = Bs + (int64_t)tb_i * bk * ldb + tn_i * RN;
+      // checked launches look at the clock between 64-step chunks of a long
+      // k-tile (the inner loop itself stays check-free)
+      const unsigned long long dlv = a.deadline ? *a.deadline : 0ull;
+      for (int kc = 0; kc < bk; kc += 64) {
+      if (a.deadline && kc && gtimer() > dlv) break;
+      const int kend = min(bk, kc + 64);
 #pragma unroll 4
-      for (int kk = 0; kk < bk; ++kk) {
+      for (int kk = kc; kk < kend; ++kk) {
         float av[RM], bv[RN];
         if constexpr (RM % 4 == 0) {
           if (a.a_vec_smem) {
@@ -319,6 +325,7 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
 #pragma unroll
           for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
       }
+      }  // 64-step chunks
       __syncthreads();
     }
     if (a.deadline) {  // finished past the deadline: a timeout (no timed repeats)

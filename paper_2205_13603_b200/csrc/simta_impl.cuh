@@ -142,8 +142,13 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
     __syncthreads();
     const float* Ap = As + tm_i * RM;
     const float* Bp = Bs + tn_i * RN;
+    // checked launches look at the clock between 64-step chunks (see simt_gemm)
+    const unsigned long long dlv = a.deadline ? *a.deadline : 0ull;
+    for (int kc = 0; kc < bk; kc += 64) {
+    if (a.deadline && kc && gtimer() > dlv) break;
+    const int kend = min(bk, kc + 64);
 #pragma unroll 4
-    for (int kk = 0; kk < bk; ++kk) {
+    for (int kk = kc; kk < kend; ++kk) {
       float av[RM], bv[RN];
 #pragma unroll
       for (int i = 0; i < RM; ++i) av[i] = Ap[kk * lda + i];
@@ -154,6 +159,7 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
 #pragma unroll
         for (int j = 0; j < RN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
+    }  // 64-step chunks
     __syncthreads();
   }
   if (a.deadline) {  // finished past the deadline: a timeout (no timed repeats)
