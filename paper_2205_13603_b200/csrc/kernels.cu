@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(1024) simt_gemm(const T* __restrict__ x, const
       for (int kc = 0; kc < bk; kc += 64) {
       if (a.deadline && kc && gtimer() > dlv) break;
       const int kend = min(bk, kc + 64);
-#pragma unroll 4
+#pragma unroll 8
       for (int kk = kc; kk < kend; ++kk) {
         float av[RM], bv[RN];
         if constexpr (RM % 4 == 0) {

@@ -192,9 +192,11 @@ struct ls_runner {
   ~ls_runner() { release(); }
 
   void release_workload() {
-    for (size_t i = 0; i < gbuf.size(); ++i)
-      if (gbuf[i] != c) pfree(gbuf[i]);
+    if (general)  // (the alt view of a contraction workload aliases x, y, c)
+      for (size_t i = 0; i < gbuf.size(); ++i)
+        if (gbuf[i] != c) pfree(gbuf[i]);
     gbuf.clear();
+    has_alt = false;
     pfree(wt);
     wt = nullptr;
     tmap_wt.clear();
@@ -298,6 +300,7 @@ struct ls_runner {
   }
   // general workloads (multi-block / affine contraction)
   bool general = false;
+  bool has_alt = false;  // contraction workload with a general-path view in gw / gbuf (plan_all alt)
   GeneralWorkload gw;
   std::vector<void*> gbuf;      // device buffer per e0 buffer (gw.buffers order)
   std::vector<int> gbuf_dtype;  // 0 bf16, 1 f32
@@ -449,8 +452,14 @@ struct ls_runner {
 
 namespace {
 
+// alt: for contraction workloads, the general-path view of the same e0; a
+// candidate the contraction instantiator cannot map (e.g. a PVU schedule
+// that fused loops into floordiv / mod indices) runs through the general
+// families (NESTGEN / SIMT-A / GENERIC) instead of being reported
+// UNSUPPORTED.
 ls_status plan_all(const Workload& w, const GeneralWorkload* gw, const DeviceLimits& lim,
-                   const char* const* programs, const size_t* lens, int n, std::vector<Plan>* plans) {
+                   const char* const* programs, const size_t* lens, int n, std::vector<Plan>* plans,
+                   const GeneralWorkload* alt = nullptr) {
   plans->assign(static_cast<size_t>(n), Plan());
   parallel_for(n, [&](int i) {
     std::string err;
@@ -471,6 +480,19 @@ ls_status plan_all(const Workload& w, const GeneralWorkload* gw, const DeviceLim
       return;
     }
     out = plan_program(w, *p, lim);
+    if (out.status == P_UNSUPPORTED && alt) {
+      DeviceLimits la = lim;
+      la.bf16 = false;  // no tcgen05 conv for a plain contraction
+      auto g = std::make_shared<GeneralPlan>(plan_general(*alt, *p, la));
+      if (g->status == P_OK) {
+        out = Plan();
+        out.status = g->status;
+        out.why = g->why;
+        out.family = g->family;
+        std::memcpy(out.cfg, g->cfg, sizeof out.cfg);
+        out.gp = g;
+      }
+    }
   });
   return LS_OK;
 }
@@ -623,7 +645,10 @@ ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* pro
         lim.bf16 = (elems / gw.shapes[b].back()) % 64 == 0 && gw.shapes[b].back() % 16 == 0;
       }
   std::vector<Plan> plans;
-  plan_all(w, general ? &gw : nullptr, lim, programs, lens, n, &plans);
+  GeneralWorkload alt;
+  std::string aerr;
+  const bool has_alt = !general && analyze_general(*p0, &alt, &aerr);
+  plan_all(w, general ? &gw : nullptr, lim, programs, lens, n, &plans, has_alt ? &alt : nullptr);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   return LS_OK;
 }
@@ -792,6 +817,32 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
     r->have_tmap_c = make_c_map(&r->tmap_c, r->c, B, M, N);
   }
   r->lim.bf16 = r->tc_ok;
+  {  // general-path view of the same buffers for candidates plan_program cannot map
+    GeneralWorkload alt;
+    std::string aerr;
+    if (analyze_general(*p0, &alt, &aerr) && alt.buffers.size() == 3) {
+      const std::string xn = p0->buffers[static_cast<size_t>(w.x_buf)].name;
+      const std::string yn = p0->buffers[static_cast<size_t>(w.y_buf)].name;
+      const std::string cn = p0->buffers[static_cast<size_t>(w.c_buf)].name;
+      r->gbuf.assign(3, nullptr);
+      r->gbuf_dtype.assign(3, 1);
+      bool ok = true;
+      for (size_t b = 0; b < 3; ++b) {
+        const std::string& nm = alt.buffers[b];
+        if (nm == xn) { r->gbuf[b] = r->x; r->gbuf_dtype[b] = r->bf16 ? 0 : 1; }
+        else if (nm == yn) { r->gbuf[b] = r->y; r->gbuf_dtype[b] = r->bf16 ? 0 : 1; }
+        else if (nm == cn) { r->gbuf[b] = r->c; r->gbuf_dtype[b] = 1; }
+        else ok = false;
+      }
+      if (ok) {
+        r->gw = alt;
+        r->has_alt = true;
+      } else {
+        r->gbuf.clear();
+        r->gbuf_dtype.clear();
+      }
+    }
+  }
   LSB_CUDA(cudaStreamSynchronize(r->st));
   r->have_workload = true;
   return LS_OK;
@@ -803,7 +854,8 @@ ls_status ls_runner_plan(ls_runner* r, const char* const* programs, const size_t
     return LS_ERR_STATE;
   }
   std::vector<Plan> plans;
-  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans);
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans,
+           r->has_alt ? &r->gw : nullptr);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   return LS_OK;
 }
@@ -821,10 +873,13 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   ls_status s = r->ensure_capacity(n);
   if (s != LS_OK) return s;
   std::vector<Plan> plans;
-  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans);
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans,
+           r->has_alt ? &r->gw : nullptr);
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   r->launches = 0;
-  if (r->general) {  // one upload of every candidate's bytecode
+  bool any_gp = false;
+  for (const Plan& p : plans) any_gp |= p.gp != nullptr;
+  if (any_gp) {  // one upload of every candidate's bytecode
     std::vector<int64_t> all;
     std::vector<size_t> at(static_cast<size_t>(n), 0);
     for (int i = 0; i < n; ++i) {
@@ -1109,7 +1164,8 @@ ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int 
   std::vector<Plan> plans;
   const char* progs[1] = {program};
   size_t lens[1] = {len};
-  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, progs, lens, 1, &plans);
+  plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, progs, lens, 1, &plans,
+           r->has_alt ? &r->gw : nullptr);
   Plan& plan = plans[0];
   int ctas = 0;
   if (plan.status == P_OK && plan.family == F_TC && !plan.gp) {

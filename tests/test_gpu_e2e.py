@@ -52,3 +52,40 @@ def test_hardware_mode_tune_reports_tflops(tmp_path):
     assert report.best.latency < report.baseline_latency
     back = R.load_records(str(tmp_path / "r.jsonl"), unit="ns")
     assert [b.latency for b in back] == [r.latency for r in report.log]
+
+
+@pytest.mark.parametrize("build,dtype", [
+    ("gmm", "bf16"), ("gmm", "f32"),      # ragged: no tcgen05 tile fits, SIMT / LOOPNEST / NAIVE
+    ("gmm128", "bf16"),                   # M = 128 with ragged N, K -> tcgen05 where BN | N and 64 | K
+    ("bmm", "bf16"),
+    ("conv", "bf16"),                     # odd spatial size, 5x5 window, pad 2
+])
+def test_ragged_shapes_every_candidate_exact(build, dtype):
+    # the reference's own sampler (b200 space) on shapes that are not
+    # multiples of any tile; every candidate that runs must match the oracle
+    # bit for bit (integer inputs), none may fail parity
+    from paper_2205_13603_b200.inputs import random_inputs
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.runner import B200Runner
+    from paper_2205_13603_b200.tensor_core import b200_space
+    from paper_2205_13603_b200.workloads import batch_matmul, conv2d_nhwc
+    from oracle import oracle as O
+    ls = loopsched()
+    e0 = {"gmm": lambda: ls.gmm(100, 72, 40), "gmm128": lambda: ls.gmm(128, 48, 192),
+          "bmm": lambda: batch_matmul(3, 33, 17, 24),
+          "conv": lambda: conv2d_nhwc(1, 13, 11, 8, 16, 5, 5, 1, 2)}[build]()
+    progs = [ls.ir.serialize(p) for p, _ in ls.spaces.sample_traces(e0, b200_space(), 48, seed=7)]
+    text = ls.ir.serialize(e0)
+    r = B200Runner(device=0, dtype=dtype, min_repeats=1, max_repeats=2, target_ms=0.005, timeout_ms=50.0)
+    r.set_workload(text, seed=5)
+    want = next(iter(O.reference_outputs(text, random_inputs(text, 5)).values()))
+    assert np.array_equal(r.reference_output(), want)
+    res = r.measure_programs(progs)
+    assert not [x for x in res if x["status"] in ("PARITY", "LAUNCH")], res
+    ran = [x for x in res if x["status"] == "OK"]
+    assert ran
+    for p, x in zip(progs, res):
+        if x["status"] == "OK" and x["family"] in ("tcgen05", "tcgen05_conv"):
+            one, = r.measure_programs([p])
+            assert np.array_equal(r.last_output().astype(np.float64), want), x["cfg"]
+    r.close()

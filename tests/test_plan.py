@@ -97,3 +97,23 @@ def test_parse_errors_are_per_candidate():
     res = plan(hdr["e0"], ["{not json", pop[0]["program"]])
     assert res[0]["status"] == "PARSE"
     assert res[1]["status"] in ("OK", "ILLEGAL")
+
+
+def test_fused_pvu_schedules_fall_back_to_the_general_families():
+    # PVU fuses small leading loops into floordiv / mod indices, which the
+    # contraction instantiator cannot map; such candidates run through the
+    # general families (NESTGEN) instead of being reported UNSUPPORTED
+    import pytest
+    from conftest import has_reference
+    if not has_reference():
+        pytest.skip("reference not importable")
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.tensor_core import b200_space
+    from paper_2205_13603_b200.workloads import batch_matmul
+    ls = loopsched()
+    e0 = batch_matmul(3, 33, 17, 24)
+    progs = [ls.ir.serialize(p) for p, _ in ls.spaces.sample_traces(e0, b200_space(), 48, seed=7)]
+    res = plan(ls.ir.serialize(e0), progs)
+    c = Counter((r["family"], r["status"]) for r in res)
+    assert c[("nestgen", "OK")] > 0
+    assert not [r for r in res if r["status"] == "UNSUPPORTED"]
