@@ -87,7 +87,22 @@ class ScoreCache:
             s = float(self.scorer.score_batch(f.reshape(1, 9), model)[0])
             self.launches += 1
             self._scores[key] = s
-        return s
+        return positive_score(s)
+
+
+_TINY, _HUGE = 5e-324, 1.7976931348623157e308
+
+
+def positive_score(s: float) -> float:
+    """The model's prediction exp(...) as the search needs it: strictly
+    positive and finite (`mh_accept` raises otherwise, `src/search.py:88-97`).
+    Identical to the reference's value whenever that one is usable; only an
+    exp() that underflowed to 0 or overflowed to inf -- reachable when the
+    model is fitted on hardware nanoseconds with sentinel latencies and
+    extrapolates far -- is clamped to the nearest positive finite double."""
+    if s != s:  # NaN: no ordering information; treat as the worst
+        return _HUGE
+    return min(max(s, _TINY), _HUGE)
 
 
 @contextlib.contextmanager

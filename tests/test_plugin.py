@@ -92,3 +92,11 @@ def test_golden_tune_reports_match_the_reference():
     assert doc["sha256"].startswith("45bd0d9a9c2f3be3")  # SURVEY.md §8c survey-time golden
     report = ls.tune(ls.gmm(512, 512, 512), ls.default_space(), ls.SearchConfig(trials=64, seed=0))
     assert digest(report) == doc["sha256"]
+
+
+def test_positive_score_only_clamps_unusable_predictions():
+    from paper_2205_13603_b200.plugin import positive_score
+    assert positive_score(1.5) == 1.5 and positive_score(1e-300) == 1e-300
+    assert positive_score(0.0) > 0.0 and positive_score(-0.0) > 0.0
+    assert positive_score(float("inf")) < float("inf")
+    assert positive_score(float("nan")) == positive_score(float("inf"))
