@@ -21,6 +21,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -58,6 +59,16 @@ EncodeTiledFn encode_fn() {
 }
 
 // bf16 K-major operand [batch][rows][K] as a 3-D TMA map with a {64, box_rows, 1} box.
+CUtensorMapL2promotion l2_promo() {  // experiment knob LSB_TMA_PROMO: 0 none, 1 64B, 2 128B, 3 256B (default)
+  static const int v = getenv("LSB_TMA_PROMO") ? atoi(getenv("LSB_TMA_PROMO")) : 3;
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, int64_t k, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
@@ -66,7 +77,7 @@ bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, 
   cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
