@@ -201,6 +201,10 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, uint32
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// the smem sources have been read (the writes complete with the grid, as in
+// CUTLASS's TMA epilogues); measured no faster here, so the kernels keep the
+// full wait unless LSB_TC_STOREWAIT=0
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // generic-proxy global writes (acquired from other CTAs) before async-proxy accesses
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -54,6 +54,7 @@ struct TcConvArgs {
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA, as tc_gemm)
   uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets + [kTcSyncSlots] zeroing flags per tile
   int tma_epi;                // modes 0/2: 128B-swizzled [64 px][32 ch] chunks -> 4-D TMA store / add-reduce
+  int full_wait;              // wait for TMA store / reduce completion before exit (LSB_TC_STOREWAIT=0: smem reads only)
   int64_t oshape[4];          // output [n][p][q][k] (decodes the box origin for the C tensor map)
 };
 
@@ -286,7 +287,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         else tma_store_4d(&tmc, src, co0 + c0, q0, p0, n0);
       }
       bulk_commit();
-      bulk_wait_all();
+      if (a.full_wait) bulk_wait_all();
+      else bulk_wait_read();
     }
   } else {
     if (warp < 2) {
@@ -372,6 +374,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   // ([n][p][q][k], row r -> (p0 + r/8, q0 + r%8)) and BN is whole 32-ch chunks
   static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
   a.tma_epi = 0;
+  static const int full_wait = getenv("LSB_TC_STOREWAIT") ? atoi(getenv("LSB_TC_STOREWAIT")) : 1;
+  a.full_wait = full_wait;
   if (tmap_c && oshape && !no_tma_epi && a.mode != 1 && g.bn % 32 == 0 && g.cc_w1 == oshape[3] &&
       g.cc_h1 == oshape[2] * oshape[3]) {
     a.tma_epi = 1;

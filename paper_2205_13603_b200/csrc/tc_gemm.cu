@@ -48,6 +48,7 @@ struct TcArgs {
   int debug;                  // experiment knob LSB_TC_DEBUG: 1 skip loads+MMA, 2 skip the epilogue,
                               // 4 skip the C stores, 8 skip the cluster exchange
   int tma_epi;                // modes 0/2, BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
+  int full_wait;              // wait for TMA store / reduce completion before exit (LSB_TC_STOREWAIT=0: smem reads only)
   int early_poll;             // mode 2: observe the zeroing flag during the main loop (LSB_TC_EARLYPOLL)
   int direct;                 // push rows from registers (st.shared::cluster) instead of staged bulk copies
   uint32_t ring_or_tile;      // bytes from the aligned base to the receive buffer
@@ -291,7 +292,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
           else tma_reduce_add_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
         }
         bulk_commit();
-        bulk_wait_all();  // complete before exit: the next launch's zeroing follows grid completion
+        if (a.full_wait) bulk_wait_all();
+        else bulk_wait_read();
       }
     } else
     for (int e = threadIdx.x; e < 128 * c4; e += 128) {
@@ -385,6 +387,8 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.direct = L.direct ? 1 : 0;
   static const int early_poll = getenv("LSB_TC_EARLYPOLL") ? atoi(getenv("LSB_TC_EARLYPOLL")) : 0;
   a.early_poll = early_poll;
+  static const int full_wait = getenv("LSB_TC_STOREWAIT") ? atoi(getenv("LSB_TC_STOREWAIT")) : 1;
+  a.full_wait = full_wait;
   static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
   a.tma_epi = L.tmap_c && !no_tma_epi && (g.mode == 0 || g.mode == 2) && L.bn % 32 == 0 ? 1 : 0;
   a.ring_or_tile = static_cast<uint32_t>(((L.direct ? g.ring : std::max(g.ring, g.tile)) + 15) & ~15LL);
