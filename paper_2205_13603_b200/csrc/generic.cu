@@ -221,6 +221,18 @@ __global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __re
 
 }  // namespace
 
+void preload_generic_kernels() {
+  cudaFuncAttributes at;
+  cudaFuncGetAttributes(&at, affcopy_kernel<__nv_bfloat16, __nv_bfloat16>);
+  cudaFuncGetAttributes(&at, affcopy_kernel<__nv_bfloat16, float>);
+  cudaFuncGetAttributes(&at, affcopy_kernel<float, __nv_bfloat16>);
+  cudaFuncGetAttributes(&at, affcopy_kernel<float, float>);
+  cudaFuncGetAttributes(&at, generic_block_kernel<float>);
+  cudaFuncGetAttributes(&at, generic_block_kernel<double>);
+  cudaFuncGetAttributes(&at, generic_nest_kernel<float>);
+  cudaGetLastError();
+}
+
 bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st) {
   const int ti = B.dtype[c.in_buf], to = B.dtype[c.out_buf];
   if (ti > 1 || to > 1) return false;

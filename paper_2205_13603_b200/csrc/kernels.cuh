@@ -47,6 +47,11 @@ void launch_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t
 void launch_transpose_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t batch, int64_t rows,
                            int64_t cols, cudaStream_t st);
 
+// Force-load every runner kernel (CUDA loads functions lazily on first use).
+void preload_simt_kernels();
+void preload_tc_gemm();
+void preload_tc_conv();
+void preload_generic_kernels();
 // Raise a kernel's dynamic smem limit to the device opt-in minus its static
 // smem; returns that limit or -1.
 int opt_in_dynamic_smem(const void* fn);

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -707,6 +708,17 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   r->lim.max_threads = prop.maxThreadsPerBlock;
   r->lim.max_smem = static_cast<int64_t>(prop.sharedMemPerBlockOptin) - 1024;
   LSB_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  {  // every runner kernel loaded now, not lazily inside a timed checked launch
+    static std::once_flag once;
+    std::call_once(once, [] {
+      preload_simt_kernels();
+      preload_simta_f32();
+      preload_simta_bf16();
+      preload_tc_gemm();
+      preload_tc_conv();
+      preload_generic_kernels();
+    });
+  }
   LSB_CUDA(cudaMalloc(&r->deadline, 8 * sizeof(unsigned long long)));
   ls_status s = r->ensure_capacity(256);
   if (s != LS_OK) return s;

@@ -28,6 +28,8 @@ struct SimtaArgs {
 };
 
 int opt_in_dynamic_smem(const void* fn);
+void preload_simta_f32();
+void preload_simta_bf16();
 bool launch_simta(const void* x, const void* y, float* c, const AffineCfg& A, bool bf16,
                   const unsigned long long* deadline, int* timed_out, cudaStream_t st);
 cudaError_t launch_simta_f32(const void* x, const void* y, float* c, const SimtaArgs& a, int rm, int rn, size_t smem,

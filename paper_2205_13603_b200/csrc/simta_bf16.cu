@@ -49,4 +49,6 @@ bool launch_simta(const void* x, const void* y, float* c, const AffineCfg& A, bo
                        : launch_simta_f32(x, y, c, a, static_cast<int>(A.rm), static_cast<int>(A.rn), smem, st);
   return e == cudaSuccess;
 }
+void preload_simta_bf16() { simta::preload_table<__nv_bfloat16>(); }
+
 }  // namespace lsb

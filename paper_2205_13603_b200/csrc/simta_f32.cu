@@ -9,4 +9,6 @@ cudaError_t launch_simta_f32(const void* x, const void* y, float* c, const Simta
   if (i < 0 || j < 0 || !t.t[i][j]) return cudaErrorInvalidValue;
   return t.t[i][j](x, y, c, a, smem, st);
 }
+void preload_simta_f32() { simta::preload_table<float>(); }
+
 }  // namespace lsb

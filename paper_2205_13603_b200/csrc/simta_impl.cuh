@@ -180,6 +180,10 @@ __global__ void __launch_bounds__(1024) simta_kernel(const T* __restrict__ x, co
 template <typename T, int RM, int RN>
 cudaError_t launch_one(const void* x, const void* y, float* c, const SimtaArgs& a, size_t smem, cudaStream_t st) {
   auto fn = simta_kernel<T, RM, RN>;
+  if (smem == static_cast<size_t>(-1)) {  // preload (see kernels.cu preload_simt_kernels)
+    cudaFuncAttributes at;
+    return cudaFuncGetAttributes(&at, fn);
+  }
   static int max_dyn = -1;
   if (max_dyn < 0) {
     max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(fn));
@@ -240,6 +244,16 @@ struct Table {
     row<T, 7>(t[5]); row<T, 8>(t[6]); row<T, 12>(t[7]); row<T, 14>(t[8]); row<T, 16>(t[9]);
   }
 };
+
+template <typename T>
+void preload_table() {
+  static Table<T> t;
+  SimtaArgs a{};
+  for (int i = 0; i < 10; ++i)
+    for (int j = 0; j < 10; ++j)
+      if (t.t[i][j]) t.t[i][j](nullptr, nullptr, nullptr, a, static_cast<size_t>(-1), nullptr);
+  cudaGetLastError();
+}
 
 }  // namespace simta
 }  // namespace lsb

@@ -334,6 +334,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
 }  // namespace
 
+void preload_tc_conv() { opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel)); }
+
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
                     cudaStream_t st, unsigned long long* trace, uint32_t* sync, const void* tmap_c,
                     const int64_t* oshape) {

@@ -360,6 +360,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
 
 }  // namespace
 
+void preload_tc_gemm() { opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_gemm_kernel)); }
+
 bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   static int max_dyn = -1;
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_gemm_kernel));
