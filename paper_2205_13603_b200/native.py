@@ -16,7 +16,8 @@ from fractions import Fraction
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libls_b200.so")
+# LSB_LIB_PATH: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("LSB_LIB_PATH") or os.path.join(HERE, "_lib", "libls_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 c_i64p = ctypes.POINTER(ctypes.c_int64)
