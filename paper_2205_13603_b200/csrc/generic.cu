@@ -80,8 +80,16 @@ template <typename Acc>
 __global__ void generic_block_kernel(GenBlock g, const int64_t* __restrict__ code, GenBuffers B,
                                      const unsigned long long* deadline, int* timed_out) {
   double vars[kGenMaxLoops];
+  int visited = 0;
   for (int64_t pt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pt < g.points;
        pt += (int64_t)gridDim.x * blockDim.x) {
+    // elementwise stages have no reduction loop to check in: look at the
+    // clock every 16 points (one interpreted point costs ~1 us)
+    if (deadline && (++visited & 15) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t > *deadline) { atomicExch(timed_out, 1); return; }
+    }
     // decode the point loops (nest order, last fastest); reduction loops start at 0
     int64_t rem = pt;
     for (int i = g.nl - 1; i >= 0; --i) {
@@ -178,12 +186,21 @@ __device__ __forceinline__ int32_t qsum(const QSum& q, const uint32_t* lv) {
 }
 
 template <typename Ti, typename To>
-__global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __restrict__ in, To* __restrict__ out) {
+__global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __restrict__ in, To* __restrict__ out,
+                               const unsigned long long* deadline, int* timed_out) {
   // thread unit: `vec` consecutive elements of the contiguous innermost run
   const uint32_t vec = static_cast<uint32_t>(c.vec);
   const uint32_t units = static_cast<uint32_t>(c.points / c.vec);
   const int outer = c.nl - c.run_loops;
+  int visited = 0;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += gridDim.x * blockDim.x) {
+    // a stage the schedule recomputes redundantly (compute_at inside loops
+    // it does not index) can be huge: checked launches look at the clock
+    if (deadline && (++visited & 15) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t > *deadline) { atomicExch(timed_out, 1); return; }
+    }
     uint32_t lv[kCopyMaxLoops];
     // digits of the run loops come from the element index inside the run
     const uint32_t per_run = static_cast<uint32_t>(c.run) / vec;
@@ -223,7 +240,7 @@ __global__ void affcopy_kernel(const __grid_constant__ CopyCfg c, const Ti* __re
 
 void preload_generic_kernels() {
   cudaFuncAttributes at;
-  cudaFuncGetAttributes(&at, affcopy_kernel<__nv_bfloat16, __nv_bfloat16>);
+  cudaFuncGetAttributes(&at, affcopy_kernel<__nv_bfloat16, __nv_bfloat16>);  // (also preloads the others below)
   cudaFuncGetAttributes(&at, affcopy_kernel<__nv_bfloat16, float>);
   cudaFuncGetAttributes(&at, affcopy_kernel<float, __nv_bfloat16>);
   cudaFuncGetAttributes(&at, affcopy_kernel<float, float>);
@@ -233,7 +250,8 @@ void preload_generic_kernels() {
   cudaGetLastError();
 }
 
-bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st) {
+bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, const unsigned long long* deadline, int* timed_out,
+                    cudaStream_t st) {
   const int ti = B.dtype[c.in_buf], to = B.dtype[c.out_buf];
   if (ti > 1 || to > 1) return false;
   const int threads = 256;
@@ -245,15 +263,15 @@ bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st) {
   const unsigned nb = static_cast<unsigned>(blocks);
   if (ti == 0 && to == 0)
     affcopy_kernel<__nv_bfloat16, __nv_bfloat16><<<nb, threads, 0, st>>>(c, static_cast<const __nv_bfloat16*>(in),
-                                                                        static_cast<__nv_bfloat16*>(out));
+                                                                        static_cast<__nv_bfloat16*>(out), deadline, timed_out);
   else if (ti == 0)
     affcopy_kernel<__nv_bfloat16, float><<<nb, threads, 0, st>>>(c, static_cast<const __nv_bfloat16*>(in),
-                                                                static_cast<float*>(out));
+                                                                static_cast<float*>(out), deadline, timed_out);
   else if (to == 0)
     affcopy_kernel<float, __nv_bfloat16><<<nb, threads, 0, st>>>(c, static_cast<const float*>(in),
-                                                                static_cast<__nv_bfloat16*>(out));
+                                                                static_cast<__nv_bfloat16*>(out), deadline, timed_out);
   else
-    affcopy_kernel<float, float><<<nb, threads, 0, st>>>(c, static_cast<const float*>(in), static_cast<float*>(out));
+    affcopy_kernel<float, float><<<nb, threads, 0, st>>>(c, static_cast<const float*>(in), static_cast<float*>(out), deadline, timed_out);
   return cudaGetLastError() == cudaSuccess;
 }
 

@@ -24,6 +24,7 @@ bool launch_generic_nest(const GenBlock& g, const int64_t* code, const GenBuffer
                          const unsigned long long* deadline, int* timed_out, cudaStream_t st);
 
 // AFFCOPY family (affine elementwise copy / pad), thread per point.
-bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, cudaStream_t st);
+bool launch_affcopy(const CopyCfg& c, const GenBuffers& B, const unsigned long long* deadline, int* timed_out,
+                    cudaStream_t st);
 
 }  // namespace lsb

@@ -382,7 +382,7 @@ struct ls_runner {
         ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace, sy, mc,
                             mc ? B.shape[stp.c_buf] : nullptr);
       } else if (stp.family == F_AFFCOPY) {
-        ok = launch_affcopy(stp.copy, B, st);
+        ok = launch_affcopy(stp.copy, B, dl, flag, st);
       } else if (stp.family == F_SIMTA) {
         ok = launch_simta(B.ptr[stp.x_buf], B.ptr[stp.y_buf], static_cast<float*>(B.ptr[stp.c_buf]), stp.aff, bf16, dl,
                           flag, st);
@@ -723,8 +723,9 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   ls_status s = r->ensure_capacity(256);
   if (s != LS_OK) return s;
   // calibrate the device-side elapsed time of an empty candidate (arm kernel,
-  // event, stamp kernel: the launch gaps a real candidate's elapsed time also
-  // carries), so the best-so-far behind every deadline is the kernel time
+  // event, one empty kernel launch, event, stamp kernel: the launch gaps a real
+  // candidate's elapsed time also carries), so the best-so-far behind every
+  // deadline is the kernel time
   {
     unsigned long long init[8] = {0, 0, ~0ull, 0, 0, 0, 0, 0};
     LSB_CUDA(cudaMemcpy(r->deadline, init, sizeof init, cudaMemcpyHostToDevice));
@@ -733,6 +734,8 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
     unsigned long long best = ~0ull;
     for (int i = 0; i < 16; ++i) {
       launch_arm(r->deadline, nullptr, nullptr, 0.0, 0, 0, r->st);
+      LSB_CUDA(cudaEventRecord(e, r->st));
+      launch_delay(0, r->st);  // stands in for the candidate's own launch
       LSB_CUDA(cudaEventRecord(e, r->st));
       launch_stamp(r->deadline, r->st);
       unsigned long long h[4];
@@ -994,6 +997,11 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   }
   for (int i = 0; i < n; ++i)
     if (out[i].status == LS_RUN_OK && !launched[static_cast<size_t>(i)]) out[i].status = LS_RUN_LAUNCH;
+  {  // diagnostics: the device-side best-so-far after phase A (debug_stats[5], us)
+    unsigned long long dev_state[5];
+    if (cudaMemcpy(dev_state, r->deadline, sizeof dev_state, cudaMemcpyDeviceToHost) == cudaSuccess)
+      r->stats[5] = dev_state[2] == ~0ull ? -1.0 : static_cast<double>(dev_state[2]) / 1e3;
+  }
   std::vector<int> tflag(static_cast<size_t>(n));
   std::vector<unsigned long long> par(static_cast<size_t>(2 * n));
   LSB_CUDA(cudaMemcpy(tflag.data(), r->flags, static_cast<size_t>(n) * sizeof(int), cudaMemcpyDeviceToHost));

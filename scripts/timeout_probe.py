@@ -8,7 +8,7 @@ from paper_2205_13603_b200.runner import B200Runner
 name = sys.argv[1] if len(sys.argv) > 1 else "bert_ffn"
 hdr, pop = load_population(name)
 dtype = "f32" if name == "gmm512" else "bf16"
-r = B200Runner(dtype=dtype, min_repeats=3, max_repeats=50, target_ms=0.02, timeout_ms=0.9, timeout_factor=10.0,
+r = B200Runner(dtype=dtype, min_repeats=3, max_repeats=50, target_ms=0.02, timeout_ms=float(os.environ.get('TMO_MS', '0.9')), timeout_factor=10.0,
                timeout_floor_ms=0.05)
 r.set_workload(hdr["e0"], seed=0)
 progs = [p["program"] for p in pop[:1024]]
