@@ -134,14 +134,29 @@ class Reader {
       if (!each()) return false;
     }
   }
+  // object keys of the interchange format never contain escapes: view them
+  // in place instead of copying each into a std::string
+  bool key(std::string_view* out) {
+    ws();
+    if (i_ >= s_.size() || s_[i_] != '"') return fail("expected string");
+    const size_t b = ++i_;
+    while (i_ < s_.size() && s_[i_] != '"') {
+      if (s_[i_] == '\\') return fail("escaped object key");
+      ++i_;
+    }
+    if (i_ >= s_.size()) return fail("unterminated string");
+    *out = s_.substr(b, i_ - b);
+    ++i_;
+    return true;
+  }
   template <class F>
   bool object(F&& each_key) {
     if (!expect('{')) return false;
     for (bool first = true;; first = false) {
       if (peek() == '}') { ++i_; return true; }
       if (!first && !expect(',')) return false;
-      std::string k;
-      if (!string(&k) || !expect(':')) return false;
+      std::string_view k;
+      if (!key(&k) || !expect(':')) return false;
       if (!each_key(k)) return false;
     }
   }
@@ -149,7 +164,7 @@ class Reader {
   bool buffers() {
     return array([&] {
       Buffer b;
-      bool ok = object([&](const std::string& k) {
+      bool ok = object([&](std::string_view k) {
         if (k == "name") return string(&b.name);
         if (k == "role") {
           std::string r;
@@ -179,19 +194,20 @@ class Reader {
   }
 
   bool expr_list(std::vector<Expr*>* out) {
+    out->reserve(4);  // operands / index lists are short: one allocation instead of up to three
     return array([&] { Expr* e = expr(); if (!e) return false; out->push_back(e); return true; });
   }
 
   Expr* expr() {
     Expr* e = p_->new_expr();
     std::string tag;
-    bool ok = object([&](const std::string& k) {
+    bool ok = object([&](std::string_view k) {
       tag = k;
       if (k == "int") { e->op = Op::Int; return integer(&e->value); }
       if (k == "var") { std::string n; if (!string(&n)) return false; e->op = Op::Var; e->var = var_id(n); return true; }
       if (k == "load") {
         e->op = Op::Load;
-        return object([&](const std::string& lk) {
+        return object([&](std::string_view lk) {
           if (lk == "buffer") { std::string n; if (!string(&n)) return false; e->buffer = buf_id(n); return good(); }
           if (lk == "indices") return expr_list(&e->kids);
           return skip_value();
@@ -215,10 +231,10 @@ class Reader {
 
   Stmt* stmt() {
     Stmt* s = p_->new_stmt();
-    bool ok = object([&](const std::string& k) {
+    bool ok = object([&](std::string_view k) {
       if (k == "loop") {
         s->type = SType::Loop;
-        return object([&](const std::string& lk) {
+        return object([&](std::string_view lk) {
           if (lk == "var") { std::string n; if (!string(&n)) return false; s->var = var_id(n); return true; }
           if (lk == "extent") return integer(&s->extent);
           if (lk == "kind") {
@@ -237,7 +253,7 @@ class Reader {
       }
       if (k == "compute") {
         s->type = SType::Compute;
-        return object([&](const std::string& ck) {
+        return object([&](std::string_view ck) {
           if (ck == "name") return string(&s->name);
           if (ck == "buffer") { std::string n; if (!string(&n)) return false; s->buffer = buf_id(n); return good(); }
           if (ck == "indices") return expr_list(&s->indices);
@@ -249,7 +265,7 @@ class Reader {
       }
       if (k == "intrinsic") {
         s->type = SType::Intrinsic;
-        return object([&](const std::string& ik) {
+        return object([&](std::string_view ik) {
           if (ik == "name") {
             std::string n;
             if (!string(&n)) return false;
@@ -266,7 +282,7 @@ class Reader {
             return array([&] {
               int buf = -1;
               std::vector<Expr*> idx;
-              bool r = object([&](const std::string& ok2) {
+              bool r = object([&](std::string_view ok2) {
                 if (ok2 == "buffer") { std::string n; if (!string(&n)) return false; buf = buf_id(n); return good(); }
                 if (ok2 == "indices") return expr_list(&idx);
                 return skip_value();
@@ -311,6 +327,8 @@ int Program::buffer_id(std::string_view name) const {
 
 std::unique_ptr<Program> parse_program(std::string_view text, std::string* err) {
   auto p = std::make_unique<Program>();
+  p->expr_pool.reserve(text.size() / 16 + 16);  // ~one node per 20-40 bytes of JSON
+  p->stmt_pool.reserve(text.size() / 128 + 8);
   Reader r(text, p.get());
   if (!r.parse_top() || !r.good()) {
     if (err) *err = r.error().empty() ? "parse error" : r.error();

@@ -989,6 +989,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     launched[static_cast<size_t>(i)] = 1;
     prev = i;
   }
+  r->stats[6] = host_now() - h0;  // phase A enqueue only (before waiting for the device)
   cudaError_t se = cudaStreamSynchronize(r->st);
   if (se != cudaSuccess) {
     cudaEventDestroy(batch0);

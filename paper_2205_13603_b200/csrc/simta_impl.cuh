@@ -198,10 +198,20 @@ cudaError_t launch_one(const void* x, const void* y, float* c, const SimtaArgs& 
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) {
-      cudaGetLastError();
-      per_sm = 1;
+    // occupancy per (threads, smem) of this instantiation, cached (the query
+    // costs host time on every checked launch otherwise)
+    static thread_local int c_threads = -1, c_per_sm = 1;
+    static thread_local size_t c_smem = 0;
+    int per_sm = c_per_sm;
+    if (threads != c_threads || smem != c_smem) {
+      per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+      }
+      c_threads = threads;
+      c_smem = smem;
+      c_per_sm = per_sm;
     }
     const int64_t wave = static_cast<int64_t>(sms) * per_sm;
     if (a.gn * a.gm > wave) {
