@@ -122,6 +122,30 @@ def test_float_inputs_tolerance():
         r.close()
 
 
+def test_float_inputs_tolerance_conv2d_and_bmm():
+    # the general path (pad stage + implicit GEMM) and batch matmul with N(0,1)
+    # inputs: bf16 rtol 2e-2 (inputs rounded once at upload, fp32 accumulation)
+    for name, fams in (("conv2d", ("tcgen05_conv", "simt_affine")), ("bmm_qk", ("tcgen05", "simt"))):
+        hdr, pop = load_population(name)
+        e0 = hdr["e0"]
+        ins = normal_inputs(e0, 11)
+        r = make_runner("bf16", rtol=2e-2, atol=1e-2, timeout_ms=50.0)
+        r.set_workload(e0, inputs=ins)
+        want = next(iter(O.reference_outputs(e0, {k: _bf16(v) for k, v in ins.items()}).values()))
+        np.testing.assert_allclose(r.reference_output(), want, rtol=1e-9, atol=1e-9)
+        progs = [p["program"] for p in pop]
+        plans = r.plan_programs(progs)
+        for fam in fams:
+            idx = pick(plans, fam, 3)
+            assert idx, fam
+            for i in idx:
+                res, = r.measure_programs([progs[i]])
+                assert res["status"] in ("OK", "TIMEOUT"), res
+                if res["status"] == "OK":
+                    np.testing.assert_allclose(r.last_output().astype(np.float64), want, rtol=2e-2, atol=1e-2)
+        r.close()
+
+
 def _bf16(v):
     import torch
     return torch.tensor(v, dtype=torch.float32).to(torch.bfloat16).to(torch.float32).numpy()
