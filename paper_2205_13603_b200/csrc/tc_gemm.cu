@@ -47,6 +47,7 @@ struct TcArgs {
   int mc;                     // cluster of N-tiles sharing A by TMA multicast (cluster dims mc x 1 x cl)
   int debug;                  // experiment knob LSB_TC_DEBUG: 1 skip loads+MMA, 2 skip the epilogue,
                               // 4 skip the C stores, 8 skip the cluster exchange
+  int reg_epi;                // mode 0, LSB_TC_REGEPI=1: registers -> global directly
   int tma_epi;                // modes 0/2, BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
   int full_wait;              // wait for TMA store / reduce completion before exit (LSB_TC_STOREWAIT=0: smem reads only)
   int early_poll;             // mode 2: observe the zeroing flag during the main loop (LSB_TC_EARLYPOLL)
@@ -227,6 +228,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
     }
     cluster_arrive();
     cluster_wait();  // every pushed row has landed
+  } else if (a.reg_epi) {
+    // mode 0 experiment (LSB_TC_REGEPI=1): rows straight from TMEM registers
+    // to global (no smem staging, no bulk-store wait before exit)
+    float* crow = a.c + batch * a.sc_b + (static_cast<int64_t>(m_blk) * 128 + row) * a.sc_m +
+                  static_cast<int64_t>(n_blk) * a.bn;
+    for (int c0 = 0; c0 < a.bn; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16_nowait(trow + c0, v);
+      tmem_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(crow + c0 + 4 * q) =
+            make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                        __uint_as_float(v[4 * q + 3]));
+    }
   } else if (a.tma_epi) {
     // TMEM -> 32-column chunks [128][32] fp32 with the 128-byte swizzle the C
     // tensor map expects (16-byte unit q of row r at q ^ (r & 7): conflict-free)
@@ -275,7 +291,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   if (tr && threadIdx.x == 0) tr[4] = gtime();
 
   const float* stile = reinterpret_cast<const float*>(gbase);
-  if (a.mode != 1) {
+  if (a.reg_epi) {
+    // stored above
+  } else if (a.mode != 1) {
     if (a.mode == 2 && !a.early_poll && s_ticket % static_cast<uint32_t>(a.parts) != 0) {
       if (threadIdx.x == 0)
         while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.parts) + 1) {
@@ -393,6 +411,8 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.full_wait = full_wait;
   static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
   a.tma_epi = L.tmap_c && !no_tma_epi && (g.mode == 0 || g.mode == 2) && L.bn % 32 == 0 ? 1 : 0;
+  static const bool reg_epi = getenv("LSB_TC_REGEPI") && atoi(getenv("LSB_TC_REGEPI")) != 0;
+  a.reg_epi = reg_epi && g.mode == 0 && !L.trace ? 1 : 0;
   a.ring_or_tile = static_cast<uint32_t>(((L.direct ? g.ring : std::max(g.ring, g.tile)) + 15) & ~15LL);
   a.sync = L.sync;
   a.trace = L.trace;
