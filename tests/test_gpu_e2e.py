@@ -12,16 +12,22 @@ from conftest import GOLDEN, needs_reference
 pytestmark = [pytest.mark.gpu, needs_reference]
 
 
-def test_parity_mode_tune_equals_reference_report():
+@pytest.mark.parametrize("name", ["gmm512", "gmm512_tu", "bert_ffn"])
+def test_parity_mode_tune_equals_reference_report(name):
     # K8 exact latencies + K7 features/scores inside the reference search:
     # the whole report (every measured trace, the chosen best trace, the
-    # refitted model's statistics) equals the CPU reference's, seed 0
-    from paper_2205_13603_b200 import plugin
+    # refitted model's statistics) equals the CPU reference's, seed 0, for
+    # the three committed tune logs (default space; with the reference's
+    # tensor_unit module; BERT FFN with the b200 space incl. use_tensor_core)
+    from paper_2205_13603_b200 import plugin, tensor_core as T
     from paper_2205_13603_b200.refapi import loopsched
     ls = loopsched()
-    want = json.load(open(os.path.join(GOLDEN, "tune_gmm512.json")))
-    report = plugin.tune(ls.gmm(512, 512, 512), ls.default_space(),
-                         ls.SearchConfig(trials=64, batch=16, population=64, seed=0), mode="parity")
+    want = json.load(open(os.path.join(GOLDEN, f"tune_{name}.json")))
+    e0, space = {"gmm512": (ls.gmm(512, 512, 512), ls.default_space_config()),
+                 "gmm512_tu": (ls.gmm(512, 512, 512),
+                               {"modules": ls.default_space_config()["modules"] + [{"tensor_unit": {}}]}),
+                 "bert_ffn": (ls.gmm(128, 768, 3072), T.b200_space_config())}[name]
+    report = plugin.tune(e0, T.space_from_config(space), ls.SearchConfig(trials=64, seed=0), mode="parity")
     got = report.to_json(timestamp=False)
     for k in ("baseline", "best", "rounds", "exhausted", "trials"):
         assert got[k] == want[k], k
