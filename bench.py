@@ -260,13 +260,20 @@ def run_b200(args):
     host_split = []
     sim_ms = []
 
+    # the batch's scoring (K7+K8 through the public API, its own stream) runs
+    # on a host thread beside the measurement: both native calls release the
+    # GIL, so their host work (parse / encode / enqueue) overlaps
+    from concurrent.futures import ThreadPoolExecutor
+    side = ThreadPoolExecutor(max_workers=1)
+
     def step():
         t0 = time.perf_counter()
         runner.set_workload(e0, inputs)
         t1 = time.perf_counter()
+        scored = side.submit(scorer.analyze, texts, model=model)
         res = runner.measure_programs(texts)
         t2 = time.perf_counter()
-        lats, feats, pred = scorer.analyze(texts, model=model)
+        lats, feats, pred = scored.result()
         wall = time.perf_counter() - t0
         st = runner.debug_stats()
         host_split.append([round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
@@ -367,7 +374,8 @@ def run_b200(args):
             "e2e": {"value": total_cands / wall_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "step_ms": [round(1e3 * w, 2) for w in walls]},
             "device_step_ms": [round(d, 2) for d in devs],
-            "host_split_ms": {"cols": ["set_workload", "measure", "analyze", "phaseA_host", "phaseB_host"],
+            "host_split_ms": {"cols": ["set_workload", "measure", "analyze (beyond measure, it runs beside it)",
+                                       "phaseA_host", "phaseB_host"],
                               "steps": host_split[-args.steps:]},
             "gpu_launches": launches,
             "clocks": clk,
