@@ -277,7 +277,8 @@ def run_b200(args):
         wall = time.perf_counter() - t0
         st = runner.debug_stats()
         host_split.append([round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
-                           round(1e3 * (time.perf_counter() - t2), 1), round(st["phase_a_host_ms"], 1), round(st["phase_b_host_ms"], 1)])
+                           round(1e3 * (time.perf_counter() - t2), 1), round(st["plan_ms"], 1), round(st["phase_a_host_ms"], 1),
+                           round(st["phase_b_host_ms"], 1)])
         devbatch.analyze(model=model)
         sim_ms.append(devbatch.elapsed_ms())
         dev_ms = runner.elapsed_ms() + sim_ms[-1]
@@ -375,7 +376,7 @@ def run_b200(args):
                     "d2h_bytes_per_step": d2h, "step_ms": [round(1e3 * w, 2) for w in walls]},
             "device_step_ms": [round(d, 2) for d in devs],
             "host_split_ms": {"cols": ["set_workload", "measure", "analyze (beyond measure, it runs beside it)",
-                                       "phaseA_host", "phaseB_host"],
+                                       "plan", "phaseA_host", "phaseB_host"],
                               "steps": host_split[-args.steps:]},
             "gpu_launches": launches,
             "clocks": clk,

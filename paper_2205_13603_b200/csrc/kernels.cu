@@ -130,6 +130,18 @@ __global__ void arm_kernel(unsigned long long* s, const int* prev_flag, const un
 
 __global__ void stamp_kernel(unsigned long long* s) { s[3] = gtimer(); }
 
+// host-released gate: waits until the host has finished enqueueing the chunk
+// of checked launches behind it (the host writes *flag >= want into mapped
+// pinned memory), so no host enqueue gap falls between a candidate's arm and
+// end stamp; gives up after max_ns so a host error path cannot hang the stream
+__global__ void gate_kernel(const volatile unsigned int* flag, unsigned int want, unsigned long long max_ns) {
+  const unsigned long long t0 = gtimer();
+  while (*flag < want) {
+    if (gtimer() - t0 > max_ns) break;
+    __nanosleep(256);
+  }
+}
+
 __global__ void delay_kernel(unsigned long long ns) {
   unsigned long long end = gtimer() + ns;
   while (gtimer() < end) {
@@ -227,6 +239,7 @@ void preload_simt_kernels() {
   cudaFuncGetAttributes(&at, parity_kernel);
   cudaFuncGetAttributes(&at, arm_kernel);
   cudaFuncGetAttributes(&at, stamp_kernel);
+  cudaFuncGetAttributes(&at, gate_kernel);
   cudaFuncGetAttributes(&at, contract_naive<__nv_bfloat16, float, float>);
   cudaFuncGetAttributes(&at, contract_naive<float, float, float>);
   cudaFuncGetAttributes(&at, loopnest_contract<__nv_bfloat16>);
@@ -317,6 +330,10 @@ void launch_arm(unsigned long long* state, const int* prev_flag, const unsigned 
 }
 
 void launch_delay(unsigned long long ns, cudaStream_t st) { delay_kernel<<<1, 1, 0, st>>>(ns); }
+
+void launch_gate(const unsigned int* flag, unsigned int want, unsigned long long max_ns, cudaStream_t st) {
+  gate_kernel<<<1, 1, 0, st>>>(flag, want, max_ns);
+}
 
 void launch_stamp(unsigned long long* state, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(state); }
 

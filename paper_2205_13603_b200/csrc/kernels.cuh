@@ -42,6 +42,8 @@ void launch_arm(unsigned long long* state, const int* prev_flag, const unsigned 
 void launch_stamp(unsigned long long* state, cudaStream_t st);
 // spin on the device for ~ns (lets the host queue a chunk of launches)
 void launch_delay(unsigned long long ns, cudaStream_t st);
+// spins until *flag >= want (mapped pinned host word) or max_ns elapsed
+void launch_gate(const unsigned int* flag, unsigned int want, unsigned long long max_ns, cudaStream_t st);
 // fp32 -> bf16 copy, and an optional 2-D transpose to make K contiguous
 void launch_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st);
 void launch_transpose_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t batch, int64_t rows,

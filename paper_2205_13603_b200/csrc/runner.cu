@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -27,6 +28,7 @@
 #include <mutex>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/loopsched_b200.h"
@@ -140,6 +142,10 @@ void fill_result(const Plan& p, ls_result* r) {
 
 }  // namespace
 
+// checked-launch gates (phase A): candidates per gated chunk, safety timeout
+constexpr int kGateChunk = 16;
+constexpr unsigned long long kGateMaxNs = 100000000ull;
+
 struct ls_runner {
   int device = 0;
   ls_runner_opts opts{};
@@ -158,6 +164,7 @@ struct ls_runner {
   CUtensorMap tmap_a{};
   CUtensorMap tmap_c{};
   bool have_tmap_c = false;
+  std::mutex map_mu;  // tensor-map caches: phase-B graphs are captured on a helper thread
   std::map<int, CUtensorMap> tmap_am;  // A maps by box rows (TMA multicast slices)
   std::map<int, CUtensorMap> tmap_b;
   unsigned long long* deadline = nullptr;  // device deadline state: [0] deadline, [1] arm time, [2] best ns
@@ -166,8 +173,12 @@ struct ls_runner {
   int cap = 0;
   std::vector<cudaEvent_t> ev;             // 4 per candidate slot
   float last_ms = 0.f;
-  int64_t launches = 0;
-  double stats[8] = {0};  // host ms phase A, host ms phase B, spin us, phase-B launches
+  std::atomic<int64_t> launches{0};
+  unsigned int* gate = nullptr;  // mapped pinned word released by the host (launch_gate)
+  unsigned int gate_seq = 0;
+  void open_gate(unsigned int v) { __atomic_store_n(gate, v, __ATOMIC_RELEASE); }
+  cudaStream_t cap_st = nullptr;  // phase-B graph capture on the helper thread (never executes)
+  double stats[8] = {0};  // host ms phase A, phase B, spin us, plan ms, empty us, best us, phase-A enqueue ms
   DeviceLimits lim;
   double launch_host_us = 4.0;  // host enqueue cost per call, for sizing the device spin
   unsigned long long empty_ns = 0;  // device elapsed of an empty candidate (arm -> stamp), calibrated
@@ -236,6 +247,10 @@ struct ls_runner {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     ev.clear();
     if (st) cudaStreamDestroy(st);
+    if (cap_st) cudaStreamDestroy(cap_st);
+    if (gate) cudaFreeHost(gate);
+    gate = nullptr;
+    cap_st = nullptr;
     st = nullptr;
   }
 
@@ -259,6 +274,7 @@ struct ls_runner {
 
   const CUtensorMap* map_a(int rows) {
     if (rows == 128) return &tmap_a;
+    std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_am.find(rows);
     if (it != tmap_am.end()) return &it->second;
     CUtensorMap m;
@@ -266,6 +282,7 @@ struct ls_runner {
     return &(tmap_am[rows] = m);
   }
   const CUtensorMap* map_b(int bn) {
+    std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_b.find(bn);
     if (it != tmap_b.end()) return &it->second;
     CUtensorMap m;
@@ -325,6 +342,7 @@ struct ls_runner {
   std::map<const void*, CUtensorMap> tmap_x;  // by activation buffer
 
   const CUtensorMap* map_wt(int bn) {
+    std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_wt.find(bn);
     if (it != tmap_wt.end()) return &it->second;
     CUtensorMap m;
@@ -333,6 +351,7 @@ struct ls_runner {
   }
   std::map<const void*, CUtensorMap> tmap_o;  // fp32 NHWC conv outputs, box {32, 8, 8, 1}
   const CUtensorMap* map_o(const void* buf, const int64_t* shape) {
+    std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_o.find(buf);
     if (it != tmap_o.end()) return &it->second;
     CUtensorMap m;
@@ -340,6 +359,7 @@ struct ls_runner {
     return &(tmap_o[buf] = m);
   }
   const CUtensorMap* map_x(const void* buf, const int64_t* shape) {
+    std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_x.find(buf);
     if (it != tmap_x.end()) return &it->second;
     CUtensorMap m;
@@ -362,7 +382,7 @@ struct ls_runner {
     return true;
   }
 
-  bool launch_general(const Plan& p, const unsigned long long* dl, int* flag, int slot) {
+  bool launch_general(const Plan& p, const unsigned long long* dl, int* flag, int slot, cudaStream_t q) {
     GenBuffers B;
     if (!general_buffers(p, &B)) return false;
     for (const GStep& stp : p.gp->steps) {
@@ -379,15 +399,15 @@ struct ls_runner {
         const CUtensorMap* mc = p.gp->gen.ndim[stp.c_buf] == 4 && B.dtype[stp.c_buf] == 1
                                     ? map_o(B.ptr[stp.c_buf], B.shape[stp.c_buf])
                                     : nullptr;
-        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, st, trace, sy, mc,
+        ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, q, trace, sy, mc,
                             mc ? B.shape[stp.c_buf] : nullptr);
       } else if (stp.family == F_AFFCOPY) {
-        ok = launch_affcopy(stp.copy, B, dl, flag, st);
+        ok = launch_affcopy(stp.copy, B, dl, flag, q);
       } else if (stp.family == F_SIMTA) {
         ok = launch_simta(B.ptr[stp.x_buf], B.ptr[stp.y_buf], static_cast<float*>(B.ptr[stp.c_buf]), stp.aff, bf16, dl,
-                          flag, st);
+                          flag, q);
       } else if (stp.family == F_NESTGEN) {
-        ok = launch_generic_nest(g, p.gcode, B, dl, flag, st);
+        ok = launch_generic_nest(g, p.gcode, B, dl, flag, q);
       } else {
         if (stp.epilogue_pass) {  // rewrite the accumulated element through the epilogue
           for (int i = 0; i < g.nl; ++i)
@@ -398,31 +418,32 @@ struct ls_runner {
           g.init_code = -1;
           g.epi_code = -1;
         }
-        ok = launch_generic_block(g, p.gcode, B, false, dl, flag, st);
+        ok = launch_generic_block(g, p.gcode, B, false, dl, flag, q);
       }
       if (!ok) return false;
     }
     return true;
   }
 
-  bool launch(const Plan& p, bool guarded, int slot) {
+  bool launch(const Plan& p, bool guarded, int slot, cudaStream_t q = nullptr) {
+    if (!q) q = st;
     const unsigned long long* dl = guarded ? deadline : nullptr;
     int* flag = flags + slot;
     if (p.gp) {
       launches += static_cast<int64_t>(p.gp->steps.size());
-      return launch_general(p, dl, flag, slot);
+      return launch_general(p, dl, flag, slot, q);
     }
     const size_t cbytes = static_cast<size_t>(w.c_elems) * sizeof(float);
-    if (p.needs_zero && cudaMemsetAsync(c, 0, cbytes, st) != cudaSuccess) return false;
+    if (p.needs_zero && cudaMemsetAsync(c, 0, cbytes, q) != cudaSuccess) return false;
     ++launches;
     switch (p.family) {
       case F_NAIVE:
-        launch_naive(x, y, c, s, bf16, st);
+        launch_naive(x, y, c, s, bf16, q);
         return cudaGetLastError() == cudaSuccess;
       case F_SIMT:
-        return launch_simt(x, y, c, s, p.simt, bf16, dl, flag, st);
+        return launch_simt(x, y, c, s, p.simt, bf16, dl, flag, q);
       case F_LOOPNEST:
-        launch_loopnest(x, y, c, p.nest, bf16, dl, flag, st);
+        launch_loopnest(x, y, c, p.nest, bf16, dl, flag, q);
         return cudaGetLastError() == cudaSuccess;
       case F_TC: {
         const CUtensorMap* mb = map_b(static_cast<int>(p.tc.bn));
@@ -454,7 +475,7 @@ struct ls_runner {
         L.sync = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
                      ? tcsync + sync_off[static_cast<size_t>(slot)]
                      : nullptr;
-        return launch_tc_gemm(L, st);
+        return launch_tc_gemm(L, q);
       }
       default:
         return false;
@@ -463,6 +484,9 @@ struct ls_runner {
 };
 
 namespace {
+
+// kernels one Runner::launch of a plan enqueues (as counted in launches)
+int64_t kernels_per_launch(const Plan& p) { return p.gp ? static_cast<int64_t>(p.gp->steps.size()) : 1; }
 
 // alt: for contraction workloads, the general-path view of the same e0; a
 // candidate the contraction instantiator cannot map (e.g. a PVU schedule
@@ -708,6 +732,9 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
   r->lim.max_threads = prop.maxThreadsPerBlock;
   r->lim.max_smem = static_cast<int64_t>(prop.sharedMemPerBlockOptin) - 1024;
   LSB_CUDA(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  LSB_CUDA(cudaStreamCreateWithFlags(&r->cap_st, cudaStreamNonBlocking));
+  LSB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&r->gate), 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  *r->gate = 0;
   {  // every runner kernel loaded now, not lazily inside a timed checked launch
     static std::once_flag once;
     std::call_once(once, [] {
@@ -733,11 +760,13 @@ ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** o
     LSB_CUDA(cudaEventCreate(&e));
     unsigned long long best = ~0ull;
     for (int i = 0; i < 16; ++i) {
+      launch_gate(r->gate, ++r->gate_seq, kGateMaxNs, r->st);
       launch_arm(r->deadline, nullptr, nullptr, 0.0, 0, 0, r->st);
       LSB_CUDA(cudaEventRecord(e, r->st));
       launch_delay(0, r->st);  // stands in for the candidate's own launch
       LSB_CUDA(cudaEventRecord(e, r->st));
       launch_stamp(r->deadline, r->st);
+      r->open_gate(r->gate_seq);
       unsigned long long h[4];
       LSB_CUDA(cudaMemcpyAsync(h, r->deadline, sizeof h, cudaMemcpyDeviceToHost, r->st));
       LSB_CUDA(cudaStreamSynchronize(r->st));
@@ -880,8 +909,10 @@ ls_status ls_runner_plan(ls_runner* r, const char* const* programs, const size_t
     return LS_ERR_STATE;
   }
   std::vector<Plan> plans;
+  const auto tp0 = std::chrono::steady_clock::now();
   plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans,
            r->has_alt ? &r->gw : nullptr);
+  const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   return LS_OK;
 }
@@ -899,8 +930,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   ls_status s = r->ensure_capacity(n);
   if (s != LS_OK) return s;
   std::vector<Plan> plans;
+  const auto tp0 = std::chrono::steady_clock::now();
   plan_all(r->w, r->general ? &r->gw : nullptr, r->lim, programs, lens, n, &plans,
            r->has_alt ? &r->gw : nullptr);
+  const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
   r->launches = 0;
   bool any_gp = false;
@@ -938,6 +971,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   auto host_now = [] { return std::chrono::duration<double, std::milli>(
                             std::chrono::steady_clock::now().time_since_epoch()).count(); };
   std::memset(r->stats, 0, sizeof r->stats);
+  r->stats[3] = plan_ms;
   r->stats[4] = static_cast<double>(r->empty_ns) / 1e3;
   double h0 = host_now();
   // ---- phase A: checked run ----
@@ -967,9 +1001,96 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
         if (plans[static_cast<size_t>(i)].status == P_OK && rank(plans[static_cast<size_t>(i)].family) == pass)
           order.push_back(i);
   }
+  // phase-B graphs of fast candidates are captured on a helper thread while
+  // the device is still running phase A: a candidate's repeat count depends
+  // only on its own checked-launch time, known once its E1 event completes.
+  // The capture stream never executes; graphs are launched on r->st in
+  // phase B (a graph that ends up unused -- timeout, single-shot -- is
+  // destroyed).
+  auto reps_for = [&](float warm_ms) {
+    double wm = std::max(1e-4, static_cast<double>(warm_ms));
+    int rep = static_cast<int>(std::ceil(r->opts.target_ms / wm));
+    return std::max(r->opts.min_repeats, std::min(r->opts.max_repeats, rep));
+  };
+  auto graph_eligible = [&](float warm_ms) {
+    return r->opts.flush_l2 == 0 && std::max(1e-4, static_cast<double>(warm_ms)) < 0.02;
+  };
+  std::vector<cudaGraphExec_t> pre_exec(static_cast<size_t>(n), nullptr);
+  std::vector<int> pre_rep(static_cast<size_t>(n), 0);
+  std::vector<char> enq_ok(static_cast<size_t>(n), 0);
+  std::atomic<int> enq_done{0};
+  std::atomic<bool> enq_stop{false};
+  std::thread helper;
+  static const bool no_precapture = getenv("LSB_NO_PRECAPTURE") && atoi(getenv("LSB_NO_PRECAPTURE")) != 0;
+  if (r->opts.flush_l2 == 0 && !order.empty() && !no_precapture) {
+    helper = std::thread([&] {
+      cudaSetDevice(r->device);
+      // start only once the enqueue loop is done: capturing beside it slows
+      // the main thread's launches (driver lock), and host gaps between an
+      // arm kernel and its candidate would inflate the checked-launch times
+      const int total = static_cast<int>(order.size());
+      while (enq_done.load(std::memory_order_acquire) < total && !enq_stop.load(std::memory_order_acquire))
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+      for (int k = 0; k < total; ++k) {
+        while (enq_done.load(std::memory_order_acquire) <= k) {
+          if (enq_stop.load(std::memory_order_acquire) && enq_done.load(std::memory_order_acquire) <= k) return;
+          std::this_thread::yield();
+        }
+        const int i = order[static_cast<size_t>(k)];
+        if (!enq_ok[static_cast<size_t>(i)]) continue;
+        if (cudaEventSynchronize(E[4 * i + 1]) != cudaSuccess) return;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, E[4 * i], E[4 * i + 1]) != cudaSuccess || !graph_eligible(ms)) continue;
+        const int rep = reps_for(ms);
+        const Plan& p = plans[static_cast<size_t>(i)];
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        bool ok = cudaStreamBeginCapture(r->cap_st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        for (int k2 = 0; ok && k2 < rep; ++k2) ok = r->launch(p, false, i, r->cap_st);
+        cudaError_t ce = cudaStreamEndCapture(r->cap_st, &g);
+        ok = ok && ce == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        if (!ok) {
+          cudaGetLastError();
+          if (ge) cudaGraphExecDestroy(ge);
+          r->launches -= kernels_per_launch(p) * rep;  // counted by launch(), never run
+          continue;
+        }
+        pre_exec[static_cast<size_t>(i)] = ge;
+        pre_rep[static_cast<size_t>(i)] = rep;
+      }
+    });
+  }
+  struct HelperJoin {  // also on an early error return out of the enqueue loop
+    std::thread& t;
+    std::atomic<bool>& stop;
+    void operator()() {
+      if (!t.joinable()) return;
+      stop.store(true, std::memory_order_release);
+      t.join();
+    }
+    ~HelperJoin() { (*this)(); }
+  } join_helper{helper, enq_stop};
+  // checked launches are enqueued in gated chunks: the device starts a chunk
+  // only once the host has enqueued all of it
+  unsigned int seq = r->gate_seq;
+  int in_chunk = 0;
   int prev = -1;
   for (int i : order) {
     const Plan& p = plans[static_cast<size_t>(i)];
+    static const bool no_gate = getenv("LSB_NO_GATE") && atoi(getenv("LSB_NO_GATE")) != 0;
+    if (in_chunk == 0 && !no_gate) {
+      launch_gate(r->gate, ++seq, kGateMaxNs, r->st);
+      ++r->launches;
+      r->gate_seq = seq;
+    }
+    if (++in_chunk == kGateChunk) in_chunk = 0;
+    struct ChunkEnd {  // opens the chunk's gate once its last candidate is enqueued (or on any exit)
+      ls_runner* r;
+      unsigned int seq;
+      bool last;
+      ~ChunkEnd() { if (last) r->open_gate(seq); }
+    } chunk_end{r, seq, in_chunk == 0};
     launch_arm(r->deadline, prev >= 0 ? r->flags + prev : nullptr, prev >= 0 ? r->parity + 2 * prev : nullptr,
                r->opts.timeout_factor, floor_ns, timeout_ns, r->st);
     ++r->launches;
@@ -981,17 +1102,39 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     if (!ok) {
       cudaGetLastError();
       out[i].status = LS_RUN_LAUNCH;
-      LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
+      enq_done.fetch_add(1, std::memory_order_release);
+      cudaError_t me = cudaMemsetAsync(r->c, 0xFF, cbytes, r->st);
+      if (me != cudaSuccess) {
+        join_helper();
+        LSB_CUDA(me);
+      }
       continue;
     }
     launch_parity(r->c, r->ref, r->w.c_elems, r->opts.rtol, r->opts.atol, r->parity + 2 * i, true, r->st);
     ++r->launches;
     launched[static_cast<size_t>(i)] = 1;
+    enq_ok[static_cast<size_t>(i)] = 1;
+    enq_done.fetch_add(1, std::memory_order_release);
     prev = i;
   }
+  r->open_gate(seq);
   r->stats[6] = host_now() - h0;  // phase A enqueue only (before waiting for the device)
+  enq_stop.store(true, std::memory_order_release);  // enqueue finished (or aborted): the helper may start
   cudaError_t se = cudaStreamSynchronize(r->st);
+  join_helper();
+  // an unused pre-captured graph: destroyed, its kernels uncounted
+  auto drop_one = [&](int i) {
+    cudaGraphExec_t& g = pre_exec[static_cast<size_t>(i)];
+    if (!g) return;
+    cudaGraphExecDestroy(g);
+    g = nullptr;
+    r->launches -= kernels_per_launch(plans[static_cast<size_t>(i)]) * pre_rep[static_cast<size_t>(i)];
+  };
+  auto drop_pre = [&] {
+    for (int i = 0; i < n; ++i) drop_one(i);
+  };
   if (se != cudaSuccess) {
+    drop_pre();
     cudaEventDestroy(batch0);
     set_error(std::string("runner phase A: ") + cudaGetErrorString(se));
     return LS_ERR_CUDA;
@@ -1065,13 +1208,16 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       if (!launched[static_cast<size_t>(i)]) continue;
       const Plan& p = plans[static_cast<size_t>(i)];
       double wm = std::max(1e-4, static_cast<double>(warm[static_cast<size_t>(i)]));
-      int rep = static_cast<int>(std::ceil(r->opts.target_ms / wm));
-      rep = std::max(r->opts.min_repeats, std::min(r->opts.max_repeats, rep));
+      const int rep = reps_for(warm[static_cast<size_t>(i)]);
       reps[static_cast<size_t>(i)] = rep;
       gpu_us += rep * wm * 1e3;
-      // graphs only where launch gaps could matter: fast candidates (the
-      // instantiation costs ~0.1 ms of host time per candidate)
-      if (r->opts.flush_l2 == 0 && wm < 0.02) {
+      if (pre_exec[static_cast<size_t>(i)] && pre_rep[static_cast<size_t>(i)] == rep) {
+        ge[static_cast<size_t>(i - c0)] = pre_exec[static_cast<size_t>(i)];  // captured during phase A
+        pre_exec[static_cast<size_t>(i)] = nullptr;
+      } else if (graph_eligible(warm[static_cast<size_t>(i)])) {
+        // graphs only where launch gaps could matter: fast candidates (the
+        // instantiation costs ~0.05 ms of host time per candidate)
+        drop_one(i);
         cudaGraph_t g = nullptr;
         bool ok = cudaStreamBeginCapture(r->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
         for (int k = 0; ok && k < rep; ++k) ok = r->launch(p, false, i);
@@ -1114,6 +1260,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     }
     prev_gpu_us = gpu_us;
   }
+  drop_pre();  // timed out / single-shot / parity-failed before phase B
   r->stats[1] = host_now() - h0;
   cudaEvent_t batch1;
   LSB_CUDA(cudaEventCreate(&batch1));
@@ -1255,8 +1402,9 @@ ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n) {
     set_error("ls_runner_debug_stats: bad arguments");
     return LS_ERR_ARG;
   }
+  const double override_us = n > 7 ? out[7] : 0.0;  // optional override (us per call)
   for (int i = 0; i < n && i < 8; ++i) out[i] = r->stats[i];
-  if (n > 7 && out[7] > 0) r->launch_host_us = out[7];  // optional override (us per call)
+  if (override_us > 0) r->launch_host_us = override_us;
   return LS_OK;
 }
 

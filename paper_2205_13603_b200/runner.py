@@ -165,7 +165,7 @@ class B200Runner:
         native.check(native.lib().ls_runner_debug_stats(self._h, native.as_np_ptr(a, ctypes.c_double), 8),
                      "debug_stats")
         return {"phase_a_host_ms": a[0], "phase_b_host_ms": a[1], "spin_us": a[2], "empty_candidate_us": a[4],
-                "device_best_us": a[5], "phase_a_enqueue_ms": a[6]}
+                "device_best_us": a[5], "phase_a_enqueue_ms": a[6], "plan_ms": a[3]}
 
     def last_output(self) -> np.ndarray:
         import json

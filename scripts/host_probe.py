@@ -1,4 +1,4 @@
-"""Host-side cost of one measure call (phase A / B host ms) for a bench slice."""
+"""Host-side cost of one measure call (plan / phase A / phase B host ms) for a bench slice."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -13,11 +13,12 @@ progs = [p["program"] for p in pop[:1024]]
 plans = r.plan_programs(progs)
 from collections import Counter
 print(Counter((p["family"], p["status"]) for p in plans))
-for it in range(3):
+for it in range(4):
     t0 = time.perf_counter()
     res = r.measure_programs(progs)
     wall = time.perf_counter() - t0
-    print(f"wall {wall*1e3:.1f} ms device {r.elapsed_ms():.1f} ms", r.debug_stats())
+    print(f"wall {wall*1e3:.1f} ms device {r.elapsed_ms():.1f} ms",
+          {k: round(v, 2) for k, v in r.debug_stats().items()})
 t0 = time.perf_counter()
 for _ in range(3):
     r.plan_programs(progs)
