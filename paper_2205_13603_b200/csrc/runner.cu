@@ -144,7 +144,7 @@ void fill_result(const Plan& p, ls_result* r) {
 
 // checked-launch gates (phase A): candidates per gated chunk, safety timeout
 constexpr int kGateChunk = 16;
-constexpr unsigned long long kGateMaxNs = 100000000ull;
+constexpr unsigned long long kGateMaxNs = 2000000ull;  // a chunk enqueues in ~0.3 ms; serialised launches (profilers) pay <= 2 ms per gate
 
 struct ls_runner {
   int device = 0;
@@ -602,9 +602,12 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
       temps.push_back(refbuf[b]);
     }
   }
-  // reference output: e0 block by block in fp64
+  LSB_CUDA(cudaStreamSynchronize(r->st));  // host inputs consumed; the rest stays queued on r->st
+  // reference output: e0 block by block in fp64 (pool blocks are reused in
+  // stream order, so the bytecode and fp64 temporaries go back to the pool
+  // while the reference run is still queued)
   int64_t* code = nullptr;
-  LSB_CUDA(cudaMalloc(&code, std::max<size_t>(gen.code.size(), 1) * 8));
+  LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&code), std::max<size_t>(gen.code.size(), 1) * 8));
   LSB_CUDA(cudaMemcpyAsync(code, gen.code.data(), gen.code.size() * 8, cudaMemcpyHostToDevice, r->st));
   GenBuffers B;
   std::memset(&B, 0, sizeof B);
@@ -618,8 +621,8 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
       set_error("reference run of e0 failed to launch");
       return LS_ERR_CUDA;
     }
-  LSB_CUDA(cudaStreamSynchronize(r->st));
-  cudaFree(code);
+  LSB_CUDA(cudaGetLastError());
+  r->pfree(code);
   for (void* t : temps) r->pfree(t);
   // K-major weight copy for the tcgen05 conv family: the contraction's
   // weight viewed as [k_rows][n_cols] (n = its contiguous last dim)
@@ -637,7 +640,6 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
                           r->wt_rows, r->wt_cols, r->st);
     LSB_CUDA(cudaGetLastError());
-    LSB_CUDA(cudaStreamSynchronize(r->st));
     r->lim.bf16 = true;
   }
   r->have_workload = true;
@@ -841,6 +843,10 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
   ls_status s;
   if ((s = upload(w.x_buf, w.x_elems, &r->x)) != LS_OK) return s;
   if ((s = upload(w.y_buf, w.y_elems, &r->y)) != LS_OK) return s;
+  // the host inputs are consumed once the uploads are done; the reference
+  // run and the operand copies below stay queued on r->st, so the first
+  // measure call plans its batch on the host while they run
+  LSB_CUDA(cudaStreamSynchronize(r->st));
   LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->c), static_cast<size_t>(w.c_elems) * 4));
   LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->ref), static_cast<size_t>(w.c_elems) * 8));
   launch_reference(r->x, r->y, r->ref, r->s, r->bf16, r->st);
@@ -898,7 +904,6 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
       }
     }
   }
-  LSB_CUDA(cudaStreamSynchronize(r->st));
   r->have_workload = true;
   return LS_OK;
 }
