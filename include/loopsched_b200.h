@@ -132,7 +132,10 @@ typedef struct ls_runner ls_runner;
 
 ls_status ls_runner_create(int device, const ls_runner_opts* opts, ls_runner** out);
 /* e0 program text plus its input tensors as float32 host arrays, in the
- * order the program declares its input buffers (random_inputs order). */
+ * order the program declares its input buffers (random_inputs order).
+ * Returns once the host arrays have been consumed (they may be freed); the
+ * fp64 reference run of e0 stays queued on the runner's stream, and a
+ * failure there is reported by the next call that waits on it. */
 ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const float* const* host_inputs,
                                  int n_inputs);
 ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const size_t* lens, int n,
