@@ -323,3 +323,29 @@ def test_single_shot_factor_skips_repeats_of_slow_candidates():
     assert all(x["latency_ns"] > 2.0 * best for x in singles)
     assert all(x["repeats"] == 3 for x in ok if x["latency_ns"] < 2.0 * best)
     r.close()
+
+
+@pytest.mark.parametrize("name,dtype", [("bert_ffn", "bf16"), ("gmm512", "f32"), ("conv2d", "bf16"),
+                                        ("conv2d", "f32")])
+def test_set_workload_consumes_host_inputs_before_returning(name, dtype):
+    """ls_runner_set_workload returns with the fp64 reference run still queued
+    (include/loopsched_b200.h): the caller's host arrays must already be
+    consumed, so overwriting them right after the call changes nothing --
+    neither the reference output nor a candidate's parity verdict."""
+    hdr, pop = load_population(name)
+    e0 = hdr["e0"]
+    ins = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in random_inputs(e0, 0).items()}
+    outs = O.reference_outputs(e0, {k: v.copy() for k, v in ins.items()})
+    want = outs["O"] if "O" in outs else next(iter(outs.values()))
+    r = make_runner(dtype, timeout_ms=200.0)
+    r.set_workload(e0, ins)
+    for v in ins.values():
+        v.fill(np.nan)   # the same buffers the C call read from
+    plans = r.plan_programs([p["program"] for p in pop[:64]])
+    ok = [i for i, p in enumerate(plans) if p["status"] == "OK"][:3]
+    res = r.measure_programs([pop[i]["program"] for i in ok])
+    assert np.array_equal(r.reference_output(), want)
+    assert all(x["status"] in ("OK", "TIMEOUT") for x in res), res
+    assert any(x["status"] == "OK" for x in res), res
+    assert all(x["mismatches"] == 0 for x in res if x["status"] == "OK"), res
+    r.close()
