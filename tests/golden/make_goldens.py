@@ -16,6 +16,11 @@ Everything written here is produced by the reference's own functions:
 * ``tune_<task>.json`` — reference ``tune`` reports (chosen trace, full log).
 * ``outputs_small.npz`` — ``random_inputs`` + ``interp.run`` outputs at small
   shapes, pinning the numpy output oracle.
+* ``replay_<task>.jsonl.gz`` — sampled traces and single-decision mutations of
+  them with the reference's ``validate_trace`` verdict (`src/trace.py:258-265`):
+  accepted -> the replayed program's ``ir.serialize`` text, structural hash
+  and normalized trace; rejected -> reason and instruction index.  The parity
+  vectors for a native trace replay.
 
 The GPU box never runs this script (the reference does not travel there); the
 fixtures do.
@@ -46,6 +51,7 @@ from loopsched.machine import MachineSpec, simulate_latency  # noqa: E402
 from loopsched.schedule import ScheduleState  # noqa: E402
 from loopsched.spaces import run_generator, sample_traces  # noqa: E402
 from loopsched.search import SearchConfig, tune  # noqa: E402
+from loopsched.trace import Accepted, mutate, serialize_trace, validate_trace  # noqa: E402
 
 SPEC = MachineSpec()
 
@@ -206,6 +212,38 @@ def write_population(name: str):
     print("population", name, len(seen), "attempts", attempts)
 
 
+def write_replay(name: str, samples: int = 48, mutations: int = 3):
+    build, space_doc, _ = POPULATIONS[name]
+    e0 = build()
+    gen = T.space_from_config(space_doc)
+    rng = random.Random(2205)
+    rows = []
+    for _ in range(samples):
+        prog, trace = run_generator(e0, gen, rng.randrange(2 ** 62))
+        rows.append({"kind": "sampled", "trace": serialize_trace(trace), "accepted": True,
+                     "program": ir.serialize(prog), "hash": ir.structural_hash(prog)})
+        for _ in range(mutations):
+            t2, pos = mutate(trace, rng)
+            if pos is None:
+                continue
+            v = validate_trace(e0, t2)
+            row = {"kind": "mutated", "mutated_index": pos, "trace": serialize_trace(t2),
+                   "accepted": isinstance(v, Accepted)}
+            if isinstance(v, Accepted):
+                row.update(program=ir.serialize(v.program), hash=ir.structural_hash(v.program),
+                           normalized=serialize_trace(v.trace))
+            else:
+                row.update(reason=v.reason, index=v.index)
+            rows.append(row)
+    path = os.path.join(HERE, f"replay_{name}.jsonl.gz")
+    with gzip.open(path, "wt") as fh:
+        fh.write(json.dumps({"workload": name, "e0": ir.serialize(e0), "space": space_doc,
+                             "seed": 2205, "rows": len(rows)}, sort_keys=True) + "\n")
+        for r in rows:
+            fh.write(json.dumps(r, sort_keys=True) + "\n")
+    print("replay", name, len(rows), "accepted", sum(r["accepted"] for r in rows))
+
+
 def write_tune(name: str, e0, space_doc, trials: int, seed: int):
     report = tune(e0, T.space_from_config(space_doc),
                   SearchConfig(trials=trials, seed=seed), SPEC)
@@ -257,3 +295,6 @@ if __name__ == "__main__":
         write_tune("bert_ffn", ls.gmm(128, 768, 3072), T.b200_space_config(), 64, 0)
     if "outputs" in what:
         write_outputs()
+    if "replay" in what:
+        for n in POPULATIONS:
+            write_replay(n)
