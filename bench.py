@@ -122,14 +122,14 @@ class ClockSampler:
 
 
 def profiled_traffic(workload):
-    """DRAM bytes per launch of the best kernel from the committed ncu --set
-    full capture (profiles/traffic.json, written by scripts/ncu_summary.py)."""
+    """(DRAM bytes per launch, source) of the best kernel from the committed
+    ncu --set full capture (profiles/traffic.json, scripts/ncu_summary.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             d = json.load(fh)[workload]
-        return {"dram_bytes_per_launch": d["dram_bytes"], "source": d["source"], "kernel": d["kernel"]}
+        return d["dram_bytes"], {"source": d["source"], "kernel": d["kernel"]}
     except Exception:
-        return None
+        return None, None
 
 
 def reference_search(e0_json, dtype, device, trials=64):
@@ -200,7 +200,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/rational",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "candidates_per_step": len(texts),
+            "config": {"workload": WORKLOADS[args.workload][2], "population": args.workload,
+                       "candidates_per_step": len(texts),
                        "path": "reference Runner simulate_latency + featurize + predict_features "
                                "(C oracle port of src/machine.py:228-254, src/costmodel.py:21-102)"},
             "note": "the reference Runner computes an analytic cost (simulate_latency) and executes no "
@@ -318,6 +319,7 @@ def run_b200(args):
     # overhead amortised over only 3 repeats; outside the timed region.
     ok = [r for r in results[-1] if r["status"] == "OK"]
     best = min(ok, key=lambda r: r["latency_ns"]) if ok else None
+    best_text = texts[results[-1].index(best)] if best else None
     best_in_step_us = best["latency_ns"] / 1e3 if best else None
     if ok:
         order = sorted(range(len(texts)), key=lambda i: results[-1][i]["latency_ns"]
@@ -337,9 +339,10 @@ def run_b200(args):
         fin.set_workload(e0, inputs)
         rem = fin.measure_programs([texts[i] for i in top])
         fin.close()
-        rem_ok = [r for r in rem if r["status"] == "OK"]
+        rem_ok = [j for j, r in enumerate(rem) if r["status"] == "OK"]
         if rem_ok:
-            best = min(rem_ok, key=lambda r: r["latency_ns"])
+            j = min(rem_ok, key=lambda j: rem[j]["latency_ns"])
+            best, best_text = rem[j], texts[top[j]]
     peak_bf16, peak_hbm, peak_src = peaks()
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
     peak = peak_bf16 if dtype == "bf16" else fp32_peak
@@ -354,11 +357,48 @@ def run_b200(args):
             fam_ms[(r["family"], r["status"])] += r["latency_ns"] * (1 + r["repeats"]) / 1e6
         elif r["status"] in ("TIMEOUT", "PARITY"):
             fam_ms[(r["family"], r["status"])] += r["latency_ns"] / 1e6
+    traffic_bytes, traffic_src = profiled_traffic(args.workload)
     h2d = sum(len(t) for t in texts) * 2 + sum(v.nbytes for v in inputs.values())
     d2h = len(texts) * (104 + 100)
 
+    # outcome accounting over every timed step of every rank
+    from paper_2205_13603_b200.dist import sum_over_ranks
+    n_all = len(texts) * args.steps
+    n_launched = sum(r["status"] in ("OK", "TIMEOUT", "PARITY") for res in results for r in res)
+    n_verdict = sum(r["status"] in ("OK", "PARITY") for res in results for r in res)
+    n_illegal = sum(r["status"] == "ILLEGAL" for res in results for r in res)
+    n_timeout = sum(r["status"] == "TIMEOUT" for res in results for r in res)
+    n_all, n_launched, n_verdict, n_illegal, n_timeout = sum_over_ranks(
+        [n_all, n_launched, n_verdict, n_illegal, n_timeout],
+        device="cuda" if args.dist_backend == "nccl" else "cpu")
+
+    # isolated single launch of the best schedule: the checked launch alone
+    # (events around one launch, L2-warm, nothing before or after it in flight)
+    isolated_us = None
+    if best is not None:
+        iso = B200Runner(device=local, dtype=dtype, min_repeats=1, max_repeats=1, target_ms=0.0,
+                         timeout_ms=timeout_ms)
+        iso.set_workload(e0, inputs)
+        vals = []
+        for _ in range(11):
+            x, = iso.measure_programs([best_text])
+            if x["status"] == "OK":
+                vals.append(x["checked_ns"] / 1e3)
+        iso.close()
+        isolated_us = statistics.median(vals) if vals else None
+
+    # parity mode end to end: the reference Runner's computation for the same
+    # slice through the public API from host program texts (ls_analyze_batch)
+    par_e2e = None
     if rank == 0:
-        cpu = cpu_baseline(progs, model, budget_s=args.cpu_budget) if world == 1 else None
+        reps, t0 = 0, time.perf_counter()
+        while reps < max(3, args.steps) or time.perf_counter() - t0 < 0.5:
+            scorer.analyze(texts, model=model)
+            reps += 1
+        par_e2e = len(texts) * reps / (time.perf_counter() - t0)
+
+    if rank == 0:
+        cpu = cpu_baseline(progs, model, budget_s=args.cpu_budget)
         search = reference_search(e0, dtype, local) if world == 1 and args.search_trials > 0 else None
         line = {
             "metric": METRIC, "value": total_cands / dev_s, "unit": "candidates/s", "n_gpus": world,
@@ -374,6 +414,14 @@ def run_b200(args):
                                   "parity": "exact (integer inputs)"}},
             "e2e": {"value": total_cands / wall_s, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "step_ms": [round(1e3 * w, 2) for w in walls]},
+            "candidates": {
+                "launched_per_s": n_launched / dev_s,
+                "completed_with_parity_verdict_per_s": n_verdict / dev_s,
+                "illegal_share": n_illegal / n_all, "timeout_share": n_timeout / n_all,
+                "what": "value counts every candidate of the slice (ILLEGAL ones are rejected by the "
+                        "instantiator without a launch; TIMEOUT ones are aborted at their deadline and "
+                        "report the abort time); launched = checked launch issued; completed = ran to the "
+                        "end and got a parity verdict"},
             "device_step_ms": [round(d, 2) for d in devs],
             "host_split_ms": {"cols": ["set_workload", "measure", "analyze (beyond measure, it runs beside it)",
                                        "plan", "phaseA_host", "phaseB_host"],
@@ -383,7 +431,8 @@ def run_b200(args):
             "best_schedule": None if best is None else {
                 "tflops": best_tflops, "frac_of_peak": best_tflops / peak,
                 "peak": peak, "peak_source": peak_src if dtype == "bf16" else "fp32 SIMT nominal",
-                "latency_us": best["latency_ns"] / 1e3, "family": best["family"], "cfg": best["cfg"],
+                "latency_us": best["latency_ns"] / 1e3, "isolated_us": isolated_us,
+                "family": best["family"], "cfg": best["cfg"],
                 "repeats": best["repeats"], "latency_us_in_step": best_in_step_us,
                 "measurement": f"top {args.final_top} distinct schedules of the last step re-measured, "
                                "CUDA graph of >= 50 back-to-back launches (>= 0.5 ms) between CUDA events",
@@ -393,13 +442,17 @@ def run_b200(args):
                 "what": "the reference Runner's own computation (simulate_latency, exact int128 rationals) + "
                         "featurize + predict for the same slice, fused K7+K8 kernel on the GPU: the like-for-like "
                         "counterpart of the --impl reference arm (which cannot execute candidates)",
-                "value": len(texts) / (statistics.median(sim_ms[-args.steps:]) / 1e3), "unit": "candidates/s"},
+                "value": len(texts) / (statistics.median(sim_ms[-args.steps:]) / 1e3), "unit": "candidates/s",
+                "e2e": par_e2e,
+                "e2e_what": "ls_analyze_batch from host program texts (parse, encode, upload, K7+K8, results "
+                            "back), host wall clock, rank 0"},
             "outcomes": {f"{a}/{b}": c for (a, b), c in sorted(fam.items())},
             "outcome_device_ms": {f"{a}/{b}": round(v, 3) for (a, b), v in sorted(fam_ms.items())},
             "roofline": None if best is None else {
                 "bound": "tensor" if dtype == "bf16" else "fp32-simt", "achieved": best_tflops,
                 "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
-                "traffic": profiled_traffic(args.workload),
+                "traffic": traffic_bytes, "traffic_source": traffic_src,
+                "frac_isolated": None if not isolated_us else flops / (isolated_us * 1e-6) / 1e12 / peak,
                 "kernel": f"best candidate ({best['family']}), L2-warm back-to-back repeats"},
             "cpu_baseline": cpu,
             "reference_search": search,
@@ -410,6 +463,18 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def spawn_ranks(n: int) -> None:
+    """``--gpus N`` without a launcher: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) and exit with its code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -431,6 +496,11 @@ def main():
     ap.add_argument("--timeout-factor", type=float, default=10.0,
                     help="checked launches get clamp(factor x best-so-far, 0.05 ms, 2 x e0) before abort")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        spawn_ranks(args.gpus)
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args)
     else:

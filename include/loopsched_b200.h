@@ -93,7 +93,10 @@ typedef struct {
   double timeout_ms;       /* device-side deadline cap for the checked launch      */
   double rtol, atol;       /* parity tolerance against the e0 reference output     */
   int32_t flush_l2;        /* reserved (must be 0)                                 */
-  int32_t reserved0;
+  int32_t carry_best;      /* nonzero: the device best-so-far behind timeout_factor */
+                           /* deadlines persists across ls_runner_measure calls of */
+                           /* one workload (small tuning batches); reset by        */
+                           /* ls_runner_set_workload                                */
   double timeout_factor;   /* >0: deadline = clamp(factor x best-so-far, floor,   */
   double timeout_floor_ms; /*      timeout_ms), tracked on the device              */
   double single_shot_factor; /* >0: a candidate whose checked launch is slower than */
@@ -126,6 +129,8 @@ typedef struct {
   double latency_ns;       /* mean device time of one launch (incl. memsets)    */
   double max_abs_err;
   int64_t mismatches;
+  double checked_ns;       /* the checked launch alone (one isolated launch     */
+                           /* between events, L2-warm, no back-to-back overlap) */
 } ls_result;
 
 typedef struct ls_runner ls_runner;

@@ -20,12 +20,27 @@ struct DModel {
 };
 
 // `predict_features`: exp(((f - mean) / scale) . w + intercept); unfit models
-// predict exp(intercept) when warm-started, else 1.
+// predict exp(intercept) when warm-started, else 1.  Every operation is
+// rounded on its own (no FMA contraction) and the dot product is summed in
+// index order; numpy's `z @ w` goes through the BLAS ddot kernel of the host,
+// whose summation order (and libm's exp) can differ in the last ulp, so this
+// is within ~1e-15 relative of the reference, not bit-identical.  Parity
+// mode re-derives the scores the search compares with the reference's own
+// formula on the host (plugin.ScoreCache(exact=True)).
 __host__ __device__ inline double score_one(const double* f, const DModel& m) {
   if (!m.is_fit) return m.n_records ? exp(m.intercept) : 1.0;
   double dot = 0.0;
-  for (int i = 0; i < 9; ++i) dot += ((f[i] - m.mean[i]) / m.scale[i]) * m.w[i];
+#ifdef __CUDA_ARCH__
+  for (int i = 0; i < 9; ++i) dot = __dadd_rn(dot, __dmul_rn(__ddiv_rn(__dsub_rn(f[i], m.mean[i]), m.scale[i]), m.w[i]));
+  return exp(__dadd_rn(dot, m.intercept));
+#else
+  for (int i = 0; i < 9; ++i) {
+    volatile double z = (f[i] - m.mean[i]) / m.scale[i];
+    volatile double p = z * m.w[i];
+    dot += p;
+  }
   return exp(dot + m.intercept);
+#endif
 }
 
 void launch_analyze(const int64_t* blobs, const int64_t* offsets, int n, const DSpec& spec, const DModel& model,

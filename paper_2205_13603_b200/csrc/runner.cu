@@ -152,6 +152,7 @@ struct ls_runner {
   cudaStream_t st = nullptr;
   bool bf16 = false;
   bool have_workload = false;
+  bool best_valid = false;  // device best-so-far initialised for this workload (carry_best)
   Workload w;
   std::string e0_text;
   bool tc_ok = false;
@@ -643,6 +644,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     r->lim.bf16 = true;
   }
   r->have_workload = true;
+  r->best_valid = false;
   return LS_OK;
 }
 
@@ -905,6 +907,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
     }
   }
   r->have_workload = true;
+  r->best_valid = false;
   return LS_OK;
 }
 
@@ -985,7 +988,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   // checked launch is armed on the device from the best time seen so far.
   std::vector<char> launched(static_cast<size_t>(n), 0);
   const unsigned long long best_init[5] = {0, 0, ~0ull, 0, r->empty_ns};
-  LSB_CUDA(cudaMemcpyAsync(r->deadline, best_init, sizeof best_init, cudaMemcpyHostToDevice, r->st));
+  if (!r->opts.carry_best || !r->best_valid) {
+    LSB_CUDA(cudaMemcpyAsync(r->deadline, best_init, sizeof best_init, cudaMemcpyHostToDevice, r->st));
+    r->best_valid = true;
+  }
   LSB_CUDA(cudaMemsetAsync(r->c, 0xFF, cbytes, r->st));
   const unsigned long long floor_ns = static_cast<unsigned long long>(r->opts.timeout_floor_ms * 1e6);
   // checked-run order: families expected to be fast first, so the device-side
@@ -1108,6 +1114,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       cudaGetLastError();
       out[i].status = LS_RUN_LAUNCH;
       enq_done.fetch_add(1, std::memory_order_release);
+      // the next arm kernel must not take this empty slot's arm-to-stamp gap
+      // as a candidate time (the last good candidate was already accounted
+      // for by this slot's own arm kernel)
+      prev = -1;
       cudaError_t me = cudaMemsetAsync(r->c, 0xFF, cbytes, r->st);
       if (me != cudaSuccess) {
         join_helper();
@@ -1159,6 +1169,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   for (int i = 0; i < n; ++i) {
     if (!launched[static_cast<size_t>(i)]) continue;
     LSB_CUDA(cudaEventElapsedTime(&warm[static_cast<size_t>(i)], E[4 * i], E[4 * i + 1]));
+    out[i].checked_ns = 1e6 * static_cast<double>(warm[static_cast<size_t>(i)]);
     double err;
     unsigned long long bits = par[static_cast<size_t>(2 * i)];
     std::memcpy(&err, &bits, sizeof err);
@@ -1170,7 +1181,10 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       out[i].repeats = 1;
       launched[static_cast<size_t>(i)] = 0;
     } else if (out[i].mismatches) {
-      out[i].status = LS_RUN_PARITY;
+      out[i].status = LS_RUN_PARITY;  // no timed repeats: latency is the checked launch
+      out[i].latency_ns = 1e6 * static_cast<double>(warm[static_cast<size_t>(i)]);
+      out[i].repeats = 0;
+      launched[static_cast<size_t>(i)] = 0;
     }
   }
 

@@ -5,7 +5,12 @@ method), each holding its own ``B200Runner`` with the workload uploaded once.
 ``ShardedRunner.measure`` deals the ordered batch round-robin by index, every
 worker measures its slice on its own stream, and the host reassembles results
 in candidate order.  There is no collective: candidates are
-independent, so the only exchange is the host-side gather.
+independent, so the only exchange is the host-side gather.  This replaces the
+reference's thread pool over one batch (`src/search.py:249-256`).
+
+Each request carries a sequence number and every worker's reply is read
+before any error is raised, so a failed call never leaves a stale reply in a
+pipe for the next call to pick up.
 """
 
 from __future__ import annotations
@@ -22,108 +27,116 @@ def deal(n: int, workers: int):
     return [list(range(w, n, workers)) for w in range(workers)]
 
 
-def _fake_result(text: str) -> dict:
-    # deterministic stand-in used by the CPU tests of the sharding logic
-    import zlib
-    return {"status": "OK", "family": "fake", "repeats": 1, "cfg": [0] * 13,
-            "latency_ns": 1000.0 + zlib.crc32(text.encode()) % 9000, "max_abs_err": 0.0, "mismatches": 0}
+def b200_factory(device: int, **opts):
+    """The production worker runner: a ``B200Runner`` on the pinned device."""
+    os.environ["CUDA_VISIBLE_DEVICES"] = str(device)
+    from .runner import B200Runner
+    return B200Runner(device=0, **opts)
 
 
-def _worker(conn, device: int, backend: str, opts: dict):
-    if backend == "b200":
-        os.environ["CUDA_VISIBLE_DEVICES"] = str(device)
-        from .runner import B200Runner
-        runner = B200Runner(device=0, **opts)
-    else:
-        runner = None
+def _worker(conn, device: int, factory, opts: dict):
+    runner = factory(device, **opts)
     try:
         while True:
-            cmd, payload = conn.recv()
+            seq, cmd, payload = conn.recv()
             if cmd == "close":
                 break
             try:
                 if cmd == "workload":
-                    if runner is not None:
-                        e0, inputs = payload
-                        runner.set_workload(e0, inputs)
-                    conn.send(("ok", None))
+                    e0, inputs = payload
+                    runner.set_workload(e0, inputs)
+                    conn.send((seq, "ok", None))
                 elif cmd == "measure":
-                    if runner is None:
-                        conn.send(("ok", [_fake_result(t) for t in payload]))
-                    else:
-                        res = runner.measure_programs(payload)
-                        conn.send(("ok", (res, runner.elapsed_ms(), runner.launch_count())))
+                    res = runner.measure_programs(payload)
+                    conn.send((seq, "ok", (res, runner.elapsed_ms(), runner.launch_count())))
                 elif cmd == "baseline":
-                    conn.send(("ok", _fake_result("e0") if runner is None else runner.baseline_result()))
+                    conn.send((seq, "ok", runner.baseline_result()))
                 else:
-                    conn.send(("err", f"unknown command {cmd}"))
+                    conn.send((seq, "err", f"unknown command {cmd}"))
             except Exception as exc:  # report, keep serving
-                conn.send(("err", repr(exc)))
+                conn.send((seq, "err", repr(exc)))
     finally:
-        if runner is not None:
-            runner.close()
+        close = getattr(runner, "close", None)
+        if close is not None:
+            close()
         conn.close()
 
 
-class ShardedRunner:
-    """Runner protocol over N GPUs (one process each)."""
+def ns_fraction(ns: float) -> Fraction:
+    return Fraction(int(round(ns * 1000.0)), 1000)
 
-    def __init__(self, devices, backend: str = "b200", sentinel_factor: float = 1e4, **opts):
+
+class ShardedRunner:
+    """Runner protocol over N GPUs (one process each).  ``factory(device,
+    **opts)`` builds each worker's runner inside the worker process (default:
+    a ``B200Runner`` pinned to that GPU)."""
+
+    def __init__(self, devices, factory=b200_factory, sentinel_factor: float = 1e4, **opts):
         self.devices = list(devices)
-        self.backend = backend
         self.sentinel_factor = sentinel_factor
         ctx = mp.get_context("spawn")
         self._conns, self._procs = [], []
         for d in self.devices:
             a, b = ctx.Pipe()
-            p = ctx.Process(target=_worker, args=(b, d, backend, opts), daemon=True)
+            p = ctx.Process(target=_worker, args=(b, d, factory, opts), daemon=True)
             p.start()
             self._conns.append(a)
             self._procs.append(p)
+        self._seq = 0
+        self._e0_text = None
         self._baseline = None
         self.last_device_ms = []
         self.last_results = []
 
-    def _call_all(self, cmd, payloads):
-        for c, pl in zip(self._conns, payloads):
-            c.send((cmd, pl))
-        out = []
-        for c in self._conns:
-            st, val = c.recv()
+    def _call(self, conns, cmd, payloads):
+        """Send one request per connection, then read EVERY reply (matched by
+        sequence number) before raising on any worker error."""
+        self._seq += 1
+        seq = self._seq
+        for c, pl in zip(conns, payloads):
+            c.send((seq, cmd, pl))
+        out, errs = [], []
+        for w, c in enumerate(conns):
+            while True:
+                rseq, st, val = c.recv()
+                if rseq == seq:
+                    break  # an older reply can only be left by an interrupted call: drop it
             if st != "ok":
-                raise RuntimeError(f"worker failed: {val}")
+                errs.append(f"worker {w} (device {self.devices[w]}): {val}")
             out.append(val)
+        if errs:
+            raise RuntimeError("worker failed: " + "; ".join(errs))
         return out
 
     def set_workload(self, e0, inputs=None) -> None:
-        self._call_all("workload", [(program_text(e0), inputs)] * len(self._conns))
+        text = program_text(e0)
+        self._call(self._conns, "workload", [(text, inputs)] * len(self._conns))
+        self._e0_text = text
         self._baseline = None
 
     def measure_programs(self, programs) -> list:
         texts = [program_text(p) for p in programs]
         slices = deal(len(texts), len(self._conns))
-        vals = self._call_all("measure", [[texts[i] for i in sl] for sl in slices])
+        vals = self._call(self._conns, "measure", [[texts[i] for i in sl] for sl in slices])
         out = [None] * len(texts)
         self.last_device_ms = []
-        for sl, v in zip(slices, vals):
-            res = v if self.backend != "b200" else v[0]
-            if self.backend == "b200":
-                self.last_device_ms.append(v[1])
+        for sl, (res, dev_ms, _launches) in zip(slices, vals):
+            self.last_device_ms.append(dev_ms)
             for i, r in zip(sl, res):
                 out[i] = r
         self.last_results = out
         return out
 
     def baseline(self, e0=None, machine_spec=None) -> Fraction:
-        if e0 is not None:
+        """Measured e0 latency on worker 0; the workload (and any custom
+        inputs) is re-uploaded only when ``e0`` differs from the loaded one."""
+        if e0 is not None and program_text(e0) != self._e0_text:
             self.set_workload(e0)
         if self._baseline is None:
-            st, r = None, None
-            self._conns[0].send(("baseline", None))
-            st, r = self._conns[0].recv()
-            if st != "ok" or r["status"] != "OK":
+            r, = self._call(self._conns[:1], "baseline", [None])
+            if r["status"] != "OK":
                 raise RuntimeError(f"baseline failed: {r}")
-            self._baseline = Fraction(int(round(r["latency_ns"] * 1000)), 1000)
+            self._baseline = ns_fraction(r["latency_ns"])
         return self._baseline
 
     def measure(self, candidates, machine_spec=None, jobs: int = 1) -> list:
@@ -132,9 +145,9 @@ class ShardedRunner:
         out = []
         for r in res:
             if r["status"] == "OK":
-                out.append(Fraction(int(round(r["latency_ns"] * 1000)), 1000))
+                out.append(ns_fraction(r["latency_ns"]))
             elif r["status"] == "TIMEOUT" and r["latency_ns"] > 0:
-                out.append(min(Fraction(int(round(r["latency_ns"] * 1000)), 1000), sentinel))
+                out.append(min(ns_fraction(r["latency_ns"]), sentinel))
             else:
                 out.append(sentinel)
         return out
@@ -142,7 +155,7 @@ class ShardedRunner:
     def close(self):
         for c in self._conns:
             try:
-                c.send(("close", None))
+                c.send((0, "close", None))
             except Exception:
                 pass
         for p in self._procs:

@@ -43,7 +43,7 @@ class RunnerOptsC(ctypes.Structure):
                 ("max_repeats", ctypes.c_int32), ("target_ms", ctypes.c_double),
                 ("timeout_ms", ctypes.c_double), ("rtol", ctypes.c_double),
                 ("atol", ctypes.c_double), ("flush_l2", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("timeout_factor", ctypes.c_double),
+                ("carry_best", ctypes.c_int32), ("timeout_factor", ctypes.c_double),
                 ("timeout_floor_ms", ctypes.c_double), ("single_shot_factor", ctypes.c_double)]
 
 
@@ -51,7 +51,7 @@ class ResultC(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("family", ctypes.c_int32),
                 ("repeats", ctypes.c_int32), ("cfg", ctypes.c_int32 * 13),
                 ("latency_ns", ctypes.c_double), ("max_abs_err", ctypes.c_double),
-                ("mismatches", ctypes.c_int64)]
+                ("mismatches", ctypes.c_int64), ("checked_ns", ctypes.c_double)]
 
 
 EXPORTS = {
@@ -187,7 +187,7 @@ def linear_model_c(model) -> LinearModelC:
 
 _RESULT_DTYPE = np.dtype([("status", np.int32), ("family", np.int32), ("repeats", np.int32),
                           ("cfg", np.int32, (13,)), ("latency_ns", np.float64), ("max_abs_err", np.float64),
-                          ("mismatches", np.int64)], align=True)
+                          ("mismatches", np.int64), ("checked_ns", np.float64)], align=True)
 
 
 def results_to_dicts(res, n):
@@ -201,8 +201,10 @@ def results_to_dicts(res, n):
     st, fam, rep = a["status"].tolist(), a["family"].tolist(), a["repeats"].tolist()
     cfg, lat = a["cfg"].tolist(), a["latency_ns"].tolist()
     err, mis = a["max_abs_err"].tolist(), a["mismatches"].tolist()
+    chk = a["checked_ns"].tolist()
     return [{"status": STATUS.get(st[i], str(st[i])), "family": FAMILY.get(fam[i], "?"), "repeats": rep[i],
-             "cfg": cfg[i], "latency_ns": lat[i], "max_abs_err": err[i], "mismatches": mis[i]}
+             "cfg": cfg[i], "latency_ns": lat[i], "max_abs_err": err[i], "mismatches": mis[i],
+             "checked_ns": chk[i]}
             for i in range(n)]
 
 

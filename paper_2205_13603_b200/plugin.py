@@ -24,6 +24,7 @@ exit even when the search raises.
 from __future__ import annotations
 
 import contextlib
+import threading
 from fractions import Fraction
 
 import numpy as np
@@ -52,10 +53,18 @@ class SimRunner:
 
 class ScoreCache:
     """K7 features memoized by program text; predictions memoized per model
-    (a new model triggers one batched K7b launch over every known row)."""
+    (a new model triggers one batched K7b launch over every known row).
 
-    def __init__(self, scorer):
+    ``exact=True`` (parity mode): the score the search compares is the
+    reference's own ``CostModel.predict_features`` (`src/costmodel.py:98-102`)
+    evaluated on the host for each new feature row, so ``mh_accept`` and the
+    (predicted, hash) ranking see bit-identical values even on near-ties
+    (numpy's ddot summation order and libm's exp are host-specific; the
+    device score agrees to ~1e-15 relative, not bitwise)."""
+
+    def __init__(self, scorer, exact: bool = False):
         self.scorer = scorer
+        self.exact = exact
         self.features: dict[str, np.ndarray] = {}
         self._model = None
         self._scores: dict[bytes, float] = {}
@@ -71,6 +80,8 @@ class ScoreCache:
         return f.copy()
 
     def predict(self, features, model) -> float:
+        if self.exact:
+            return positive_score(model.predict_features(np.asarray(features, dtype=np.float64)))
         if model is not self._model:
             self._model = model
             self._scores = {}
@@ -105,24 +116,86 @@ def positive_score(s: float) -> float:
     return min(max(s, _TINY), _HUGE)
 
 
+class _Seams:
+    """What one ``installed()`` block routes the reference's seams to."""
+
+    def __init__(self, runner, cache):
+        self.runner = runner
+        self.cache = cache
+
+
+_tls = threading.local()
+_install_lock = threading.Lock()
+_install_depth = 0
+_originals = None
+
+
+def _current():
+    st = getattr(_tls, "stack", None)
+    return st[-1] if st else None
+
+
+def _d_measure(cands, spec, jobs):
+    cur = _current()
+    if cur is not None and cur.runner is not None:
+        return cur.runner.measure(cands, spec, jobs)
+    return _originals[0](cands, spec, jobs)
+
+
+def _d_simulate(p, spec=None):
+    cur = _current()
+    if cur is not None and cur.runner is not None:
+        return cur.runner.baseline(p, spec)
+    return _originals[1](p, spec) if spec is not None else _originals[1](p)
+
+
+def _d_featurize(p, spec=None):
+    cur = _current()
+    if cur is not None and cur.cache is not None:
+        return cur.cache.featurize(p, spec)
+    return _originals[2](p, spec) if spec is not None else _originals[2](p)
+
+
+def _d_predict(self, program, features, model):
+    cur = _current()
+    if cur is not None and cur.cache is not None:
+        return cur.cache.predict(features, model)
+    return _originals[3](self, program, features, model)
+
+
 @contextlib.contextmanager
-def installed(runner=None, scorer=None):
-    """Rebind the reference's seams to ``runner`` (Runner protocol) and
-    ``scorer`` (Scorer protocol) inside the block."""
+def installed(runner=None, scorer=None, exact_scores: bool = False):
+    """Route the reference's seams to ``runner`` (Runner protocol) and
+    ``scorer`` (Scorer protocol) inside the block.
+
+    The module-level seams are rebound once to dispatchers that look up the
+    innermost ``installed()`` block of the CALLING THREAD (falling back to the
+    reference's originals), so concurrent tunes on several threads -- e.g. one
+    per GPU -- each see their own runner; the originals are restored when the
+    last block exits, also when the search raises."""
+    global _install_depth, _originals
     ls = loopsched()
     S = ls.search
-    saved = (S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict)
-    cache = ScoreCache(scorer) if scorer is not None else None
+    cache = ScoreCache(scorer, exact=exact_scores) if scorer is not None else None
+    with _install_lock:
+        if _install_depth == 0:
+            _originals = (S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict)
+            S._measure_batch, S.simulate_latency, S.featurize = _d_measure, _d_simulate, _d_featurize
+            S._Validator._predict = _d_predict
+        _install_depth += 1
+    st = getattr(_tls, "stack", None)
+    if st is None:
+        st = _tls.stack = []
+    st.append(_Seams(runner, cache))
     try:
-        if runner is not None:
-            S._measure_batch = lambda cands, spec, jobs: runner.measure(cands, spec, jobs)
-            S.simulate_latency = lambda p, spec=None: runner.baseline(p, spec)
-        if cache is not None:
-            S.featurize = lambda p, spec=None: cache.featurize(p, spec)
-            S._Validator._predict = lambda self, program, features, model: cache.predict(features, model)
         yield cache
     finally:
-        S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict = saved
+        st.pop()
+        with _install_lock:
+            _install_depth -= 1
+            if _install_depth == 0:
+                S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict = _originals
+                _originals = None
 
 
 def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
@@ -148,7 +221,7 @@ def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
             runner.set_workload(e0)
         else:
             raise ValueError(f"unknown mode {mode!r}")
-    with installed(runner, scorer):
+    with installed(runner, scorer, exact_scores=(mode == "parity")):
         return ls.search.tune(e0, generator, config, machine_spec, warm_records)
 
 

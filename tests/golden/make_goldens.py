@@ -178,11 +178,16 @@ def write_programs():
 
 
 POPULATIONS = {
-    # name: (builder, space-config, size)
+    # name: (builder, space-config, size); 8192 = 8 GPUs x 1024 distinct
+    # candidates per rank for the four bench workloads (disjoint rank slices
+    # at every N), 1024 for the other config-5 tasks
     "bert_ffn": (lambda: ls.gmm(128, 768, 3072), T.b200_space_config(), 8192),
-    "bmm_qk": (lambda: W.batch_matmul(12, 128, 128, 64), T.b200_space_config(), 1024),
-    "gmm512": (lambda: ls.gmm(512, 512, 512), ls.default_space_config(), 1024),
-    "conv2d": (lambda: W.conv2d_nhwc(), T.b200_space_config(), 512),
+    "bmm_qk": (lambda: W.batch_matmul(12, 128, 128, 64), T.b200_space_config(), 8192),
+    "gmm512": (lambda: ls.gmm(512, 512, 512), ls.default_space_config(), 8192),
+    "conv2d": (lambda: W.conv2d_nhwc(), T.b200_space_config(), 8192),
+    "bert_dense": (lambda: ls.gmm(128, 768, 768), T.b200_space_config(), 1024),
+    "bert_ffn_in": (lambda: ls.gmm(128, 3072, 768), T.b200_space_config(), 1024),
+    "bmm_pv": (lambda: W.batch_matmul(12, 128, 64, 128), T.b200_space_config(), 1024),
 }
 
 
@@ -280,12 +285,49 @@ def write_outputs():
     print("outputs", len(arrays))
 
 
+BIG_OUTPUT_CASES = {
+    # the BASELINE config shapes incl. every config-5 task
+    "gmm512": lambda: ls.gmm(512, 512, 512),
+    "bert_ffn": lambda: ls.gmm(128, 768, 3072),
+    "bert_dense": lambda: ls.gmm(128, 768, 768),
+    "bert_ffn_in": lambda: ls.gmm(128, 3072, 768),
+    "bmm_qk": lambda: W.batch_matmul(12, 128, 128, 64),
+    "bmm_pv": lambda: W.batch_matmul(12, 128, 64, 128),
+    "conv2d": lambda: W.conv2d_nhwc(),
+}
+
+
+def write_outputs_big():
+    """sha256 of the reference interpreter's own inputs and outputs
+    (`interp.random_inputs(e0, 0)`, `interp.run`, `src/interp.py:54-63`,
+    `:314-342`) at the full BASELINE shapes, as int64 C-order bytes: pins the
+    numpy output oracle (oracle.reference_outputs) and the repo's
+    random_inputs at the sizes the GPU parity tests run."""
+    from loopsched import interp
+    doc = {}
+    for name, build in BIG_OUTPUT_CASES.items():
+        e0 = build()
+        inp = interp.random_inputs(e0, 0)
+        out = interp.run(e0, inp)
+        sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+        doc[name] = {"e0": ir.serialize(e0), "seed": 0,
+                     "inputs": {k: sha(v.as_array()) for k, v in inp.items()},
+                     "outputs": {k: {"sha256": sha(v.as_array()), "shape": list(v.as_array().shape),
+                                     "max_abs": int(np.abs(v.as_array()).max())} for k, v in out.items()}}
+        print("outputs_big", name, {k: v["max_abs"] for k, v in doc[name]["outputs"].items()})
+    with open(os.path.join(HERE, "outputs_big.json"), "w") as fh:
+        json.dump(doc, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["programs", "pops", "tune", "outputs"]
     if "programs" in what:
         write_programs()
     if "pops" in what:
         for n in POPULATIONS:
+            write_population(n)
+    for n in POPULATIONS:
+        if f"pop:{n}" in what:
             write_population(n)
     if "tune" in what:
         write_tune("gmm512", ls.gmm(512, 512, 512), ls.default_space_config(), 64, 0)
@@ -295,6 +337,8 @@ if __name__ == "__main__":
         write_tune("bert_ffn", ls.gmm(128, 768, 3072), T.b200_space_config(), 64, 0)
     if "outputs" in what:
         write_outputs()
+    if "outputs_big" in what:
+        write_outputs_big()
     if "replay" in what:
         for n in POPULATIONS:
             write_replay(n)

@@ -129,7 +129,7 @@ def test_float_inputs_tolerance_conv2d_and_bmm():
         hdr, pop = load_population(name)
         e0 = hdr["e0"]
         ins = normal_inputs(e0, 11)
-        r = make_runner("bf16", rtol=2e-2, atol=1e-2, timeout_ms=50.0)
+        r = make_runner("bf16", rtol=2e-2, atol=1e-2, timeout_ms=1000.0)
         r.set_workload(e0, inputs=ins)
         want = next(iter(O.reference_outputs(e0, {k: _bf16(v) for k, v in ins.items()}).values()))
         np.testing.assert_allclose(r.reference_output(), want, rtol=1e-9, atol=1e-9)
@@ -137,12 +137,11 @@ def test_float_inputs_tolerance_conv2d_and_bmm():
         plans = r.plan_programs(progs)
         for fam in fams:
             idx = pick(plans, fam, 3)
-            assert idx, fam
-            for i in idx:
+            assert len(idx) == 3, fam
+            for i in idx:   # every pick must run to completion and pass
                 res, = r.measure_programs([progs[i]])
-                assert res["status"] in ("OK", "TIMEOUT"), res
-                if res["status"] == "OK":
-                    np.testing.assert_allclose(r.last_output().astype(np.float64), want, rtol=2e-2, atol=1e-2)
+                assert res["status"] == "OK", res
+                np.testing.assert_allclose(r.last_output().astype(np.float64), want, rtol=2e-2, atol=1e-2)
         r.close()
 
 
@@ -223,7 +222,7 @@ def test_conv2d_general_path_bit_exact(dtype):
     import json
     hdr, pop = load_population("conv2d")
     e0 = hdr["e0"]
-    r = make_runner(dtype, timeout_ms=200.0)
+    r = make_runner(dtype, timeout_ms=2000.0)
     r.set_workload(e0, seed=0)
     want = O.reference_outputs(e0, random_inputs(e0, 0))["O"]
     assert np.array_equal(r.reference_output(), want)
@@ -232,15 +231,16 @@ def test_conv2d_general_path_bit_exact(dtype):
     inlined = [i for i, p in enumerate(progs)
                if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
     picks = pick(plans, "simt_affine", 6) + inlined[:4] + pick(plans, "nestgen", 1)
+    assert len(pick(plans, "simt_affine", 6)) == 6 and len(inlined) >= 4
     if dtype == "bf16":
-        picks += [i for i, x in enumerate(plans) if x["family"] == "tcgen05_conv"]
-    assert picks
-    for i in picks:
+        tc = [i for i, x in enumerate(plans) if x["family"] == "tcgen05_conv"]
+        assert len(tc) >= 4
+        picks += tc
+    for i in picks:   # every pick must finish (2 s cap) and be bit-exact
         res, = r.measure_programs([progs[i]])
-        assert res["status"] in ("OK", "TIMEOUT"), res
-        if res["status"] == "OK":
-            assert res["mismatches"] == 0, res
-            assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
+        assert res["status"] == "OK", res
+        assert res["mismatches"] == 0, res
+        assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
     base = r.baseline_result()
     assert base["status"] == "OK" and base["mismatches"] == 0
     r.close()
@@ -252,12 +252,12 @@ def test_conv2d_population_slice_has_no_parity_failures():
     # the in-run parity reducer flags no candidate
     hdr, pop = load_population("conv2d")
     e0 = hdr["e0"]
-    r = make_runner("bf16", timeout_ms=5.0, timeout_factor=10.0)
+    r = make_runner("bf16", timeout_ms=20.0)
     r.set_workload(e0, seed=0)
     res = r.measure_programs([p["program"] for p in pop[:384]])
     bad = [x for x in res if x["status"] in ("PARITY", "LAUNCH")]
     assert not bad, bad[:3]
-    assert sum(x["status"] == "OK" for x in res) > 20
+    assert sum(x["status"] == "OK" for x in res) > 50
     r.close()
 
 
@@ -294,7 +294,7 @@ def test_sharded_runner_b200_workers_match_single_runner():
     one.set_workload(e0, seed=0)
     want = one.measure_programs(progs)
     one.close()
-    sh = ShardedRunner([0, 0], backend="b200", dtype="bf16", min_repeats=1, max_repeats=3, target_ms=0.005,
+    sh = ShardedRunner([0, 0], dtype="bf16", min_repeats=1, max_repeats=3, target_ms=0.005,
                        timeout_ms=5.0)
     try:
         sh.set_workload(e0)

@@ -5,6 +5,7 @@ import os
 import pytest
 import torch.multiprocessing as tmp
 
+from fake_runner import fake_factory
 from paper_2205_13603_b200 import dist, multigpu
 
 
@@ -19,8 +20,8 @@ def test_deal_covers_each_index_once():
 
 def test_sharded_runner_reassembles_in_order():
     texts = [f'{{"buffers": [], "root": [], "i": {i}}}' for i in range(23)]
-    one = multigpu.ShardedRunner([0], backend="fake")
-    three = multigpu.ShardedRunner([0, 1, 2], backend="fake")
+    one = multigpu.ShardedRunner([0], factory=fake_factory)
+    three = multigpu.ShardedRunner([0, 1, 2], factory=fake_factory)
     try:
         a = one.measure_programs(texts)
         b = three.measure_programs(texts)
@@ -30,6 +31,27 @@ def test_sharded_runner_reassembles_in_order():
     finally:
         one.close()
         three.close()
+
+
+def test_worker_error_drains_every_reply():
+    # one worker fails: every reply is read before raising, so the next call
+    # gets fresh answers (no stale reply left in a pipe)
+    texts = [f"prog-{i}" for i in range(8)]
+    sh = multigpu.ShardedRunner([0, 1], factory=fake_factory, fail_on="prog-3")
+    try:
+        with pytest.raises(RuntimeError, match="injected failure"):
+            sh.measure_programs(texts)
+        good = [f"ok-{i}" for i in range(6)]
+        got = sh.measure_programs(good)
+        assert [r["latency_ns"] for r in got] == [fake_factory(0)._result(t)["latency_ns"] for t in good]
+        # baseline() with the loaded e0 does not re-upload (custom inputs stay)
+        sh.set_workload('{"e0": 1}')
+        sh.baseline('{"e0": 1}')
+        assert sh.measure_programs(["x"])[0]["workloads"] == 1
+        sh.baseline('{"e0": 2}')
+        assert sh.measure_programs(["x"])[0]["workloads"] == 2
+    finally:
+        sh.close()
 
 
 def test_rank_slices_are_disjoint():

@@ -66,3 +66,27 @@ def test_output_oracle_matches_interpreter():
             got = O.reference_outputs(e0, ins)
             for k, v in outs.items():
                 assert np.array_equal(got[k].astype(np.int64), v), (name, seed, k)
+
+
+def test_output_oracle_pinned_at_baseline_shapes():
+    """The numpy output oracle and the repo's random_inputs at the full
+    BASELINE shapes (every config-5 task included) against sha256 hashes of
+    the reference interpreter's own inputs and outputs
+    (tests/golden/outputs_big.json, made by make_goldens.py outputs_big from
+    `interp.random_inputs` / `interp.run`, `src/interp.py:54-63`, `:314-342`)."""
+    import hashlib
+    import json
+    from paper_2205_13603_b200.inputs import random_inputs
+    with open(os.path.join(GOLDEN, "outputs_big.json")) as fh:
+        doc = json.load(fh)
+    assert len(doc) == 7
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+    for name, case in doc.items():
+        ins = random_inputs(case["e0"], case["seed"])
+        assert {k: sha(v) for k, v in ins.items()} == case["inputs"], name
+        got = O.reference_outputs(case["e0"], ins)
+        for k, want in case["outputs"].items():
+            v = got[k]
+            assert list(v.shape) == want["shape"], name
+            assert np.array_equal(v, np.round(v)) and np.abs(v).max() == want["max_abs"], name
+            assert sha(v) == want["sha256"], (name, k)

@@ -61,3 +61,59 @@ def test_gradient_prefers_heavier_identical_task():
     sch = TaskScheduler(tasks, 96, round_trials=16, batch=8, population=16, seed=5, tune_fn=ref_tune())
     sch.run()
     assert tasks[1].trials > tasks[0].trials
+
+
+def test_repeat_schedules_are_cached_and_not_counted():
+    # later rounds restart the reference tune with an empty measured set: a
+    # repeated program is answered from the task's records (no new
+    # measurement) and only new programs count toward the budget
+    from paper_2205_13603_b200.task_scheduler import CachingRunner, _CountingSimRunner
+    sch = make(96, seed=2)
+    sch.run()
+    for t in sch.tasks:
+        hashes = [r.program_hash for r in t.records]
+        assert len(hashes) == len(set(hashes))            # warm records de-duplicated
+        assert t.trials == len(t.records)                 # budget counts distinct programs only
+    assert sch.spent == sum(t.trials for t in sch.tasks) <= 96
+
+    class Cand:
+        def __init__(self, h, p):
+            self.program_hash, self.program = h, p
+    from paper_2205_13603_b200.refapi import loopsched
+    ls = loopsched()
+    p = ls.gmm(8, 8, 8)
+    c = CachingRunner(_CountingSimRunner(), {1: 5})
+    out = c.measure([Cand(1, p), Cand(2, p), Cand(2, p)])
+    assert out[0] == 5 and out[1] == out[2] == ls.simulate_latency(p, ls.MachineSpec()) and c.fresh == 2
+
+
+def test_parallel_waves_are_deterministic():
+    # task-parallel allocation (one task per GPU in waves): identical however
+    # the workers' completion order falls, and identical across runs
+    import random
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+
+    def submitter(delays):
+        pool = ThreadPoolExecutor(max_workers=4)
+        rnd = random.Random(delays)
+
+        def submit(sched, t, cfg):
+            d = rnd.random() * 0.05
+
+            def job():
+                time.sleep(d)   # scramble completion order
+                return sched.execute_round(t, cfg)
+            return pool.submit(job)
+        return submit, pool
+
+    outs = []
+    for k in range(2):
+        sub, pool = submitter(k)
+        s = make(160, seed=4).run(parallel=4, submit=sub)
+        pool.shutdown()
+        outs.append(s)
+    a, b = outs
+    assert [(r["task"], r["trials"]) for r in a["allocation"]] == [(r["task"], r["trials"]) for r in b["allocation"]]
+    assert a["objective_exact"] == b["objective_exact"] and a["trials"] <= 160
+    assert all(t["rounds"] >= 1 for t in a["tasks"])
