@@ -230,7 +230,11 @@ def test_conv2d_general_path_bit_exact(dtype):
     plans = r.plan_programs(progs)
     inlined = [i for i, p in enumerate(progs)
                if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
-    picks = pick(plans, "simt_affine", 6) + inlined[:4] + pick(plans, "nestgen", 1)
+    # the nest-generic candidate with the most threads (its outermost parallel
+    # loop): one with 56 threads runs the whole conv in ~56 threads (> 2 s)
+    ng = sorted((i for i, x in enumerate(plans) if x["family"] == "nestgen" and x["status"] == "OK"),
+                key=lambda i: -plans[i]["cfg"][0])
+    picks = pick(plans, "simt_affine", 6) + inlined[:4] + ng[:1]
     assert len(pick(plans, "simt_affine", 6)) == 6 and len(inlined) >= 4
     if dtype == "bf16":
         tc = [i for i, x in enumerate(plans) if x["family"] == "tcgen05_conv"]
