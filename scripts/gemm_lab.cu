@@ -105,7 +105,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       for (int kt = 0; kt < p.KT; ++kt) {
         const int kc = (split * p.KT + kt) * 64;
         mbar_expect_tx(full + 8 * kt, kA + bbytes);
-        if (p.CN > 1)
+        if (p.CN > 1)  // ta's box is {64, 128 / CN}: my row slice, into every CTA of the cluster
           tma_load_3d_mc(a0 + kt * kA + rank * rows * 128, &ta, full + 8 * kt, kc, rank * rows, 0, mask);
         else
           tma_load_3d(a0 + kt * kA, &ta, full + 8 * kt, kc, 0, 0);
@@ -241,6 +241,34 @@ static uint16_t f2bf(float f) {
 
 int main(int argc, char** argv) {
   const int M = 128, N = 768, K = 3072;
+  struct V { int BN, S, CN, red, skip; };
+  std::vector<V> vs;
+  const int bns[] = {32, 48, 64, 96, 128, 192, 256};
+  for (int bn : bns)
+    for (int S : {1, 2, 3, 4, 6, 8, 12, 16, 24, 48}) {
+      const int ctas = (N / bn) * S;
+      if (ctas < 48 || ctas > 296) continue;
+      for (int cn : {1, 2, 4})
+        for (int red : {0, 1}) {
+          if ((N / bn) % cn) continue;
+          if (S == 1 && red == 1) continue;
+          if (red == 1 && ctas > 148) continue;  // co-residency of a tile's splits (1 CTA/SM worst case)
+          vs.push_back({bn, S, cn, red, 0});
+        }
+    }
+  if (argc == 6) {  // one variant: BN S CN red skip
+    vs.clear();
+    vs.push_back({atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5])});
+  }
+  if (argc == 2) {  // list the default variants
+    for (const V& v : vs) printf("%d %d %d %d %d\n", v.BN, v.S, v.CN, v.red, v.skip);
+    return 0;
+  }
+  // decomposition of the best-known config
+  vs.push_back({32, 12, 1, 0, 2});
+  vs.push_back({32, 12, 1, 0, 3});
+  vs.push_back({64, 12, 1, 0, 2});
+  vs.push_back({64, 12, 2, 0, 2});
   std::vector<uint16_t> ha(M * K), hb(N * K);
   std::vector<float> fa(M * K), fb(N * K);
   uint32_t s = 12345;
@@ -276,7 +304,8 @@ int main(int argc, char** argv) {
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
   CK(cudaFuncSetAttribute(lab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 64));
   CK(cudaFuncSetAttribute(lab_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  CUtensorMap tma = map3(da, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 1, 64, 128);
+  CUtensorMap tma_cn[5];
+  for (int cn : {1, 2, 4}) tma_cn[cn] = map3(da, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, M, 1, 64, 128 / cn);
   CUtensorMap tmc = map3(dc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, N, M, 1, 32, 128);
   CUtensorMap tmw = map3(dws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, N, M, 64, 32, 128);
   cudaStream_t st;
@@ -287,27 +316,7 @@ int main(int argc, char** argv) {
   void* scrub;
   CK(cudaMalloc(&scrub, 256 << 20));
 
-  struct V { int BN, S, CN, red, skip; };
-  std::vector<V> vs;
-  const int bns[] = {32, 48, 64, 96, 128, 192, 256};
-  for (int bn : bns)
-    for (int S : {1, 2, 3, 4, 6, 8, 12, 16, 24, 48}) {
-      const int ctas = (N / bn) * S;
-      if (ctas < 48 || ctas > 296) continue;
-      for (int cn : {1, 2, 4})
-        for (int red : {0, 1}) {
-          if ((N / bn) % cn) continue;
-          if (S == 1 && red == 1) continue;
-          if (red == 1 && ctas > 148) continue;  // co-residency of a tile's splits (1 CTA/SM worst case)
-          vs.push_back({bn, S, cn, red, 0});
-        }
-    }
-  // decomposition of the best-known config
-  vs.push_back({32, 12, 1, 0, 2});
-  vs.push_back({32, 12, 1, 0, 3});
-  vs.push_back({64, 12, 1, 0, 2});
-  vs.push_back({64, 12, 2, 0, 2});
-  printf("BN S CN red skip ctas smemKB | graph_us iso_us exact\n");
+  if (argc != 6) printf("BN S CN red skip ctas smemKB | graph_us iso_us exact\n");
   for (const V& v : vs) {
     P p{};
     p.N = N;
@@ -348,6 +357,7 @@ int main(int argc, char** argv) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
+    const CUtensorMap tma = tma_cn[v.CN];
     auto launch = [&]() { return cudaLaunchKernelEx(&cfg, lab_kernel, tma, tmb, tmc, tmw, p); };
     if (launch() != cudaSuccess) {
       printf("%d %d %d %d %d launch failed: %s\n", v.BN, v.S, v.CN, v.red, v.skip, cudaGetErrorString(cudaGetLastError()));

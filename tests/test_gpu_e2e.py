@@ -90,6 +90,8 @@ def test_ragged_shapes_every_candidate_exact(build, dtype):
     assert not [x for x in res if x["status"] in ("PARITY", "LAUNCH")], res
     ran = [x for x in res if x["status"] == "OK"]
     assert ran
+    if build == "conv":  # the interpreted nest-generic family runs to completion here
+        assert sum(x["family"] == "nestgen" for x in ran) >= 10, [x["status"] for x in res]
     for p, x in zip(progs, res):
         if x["status"] == "OK" and x["family"] in ("tcgen05", "tcgen05_conv"):
             one, = r.measure_programs([p])

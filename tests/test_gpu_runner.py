@@ -230,11 +230,10 @@ def test_conv2d_general_path_bit_exact(dtype):
     plans = r.plan_programs(progs)
     inlined = [i for i, p in enumerate(progs)
                if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
-    # the nest-generic candidate with the most threads (its outermost parallel
-    # loop): one with 56 threads runs the whole conv in ~56 threads (> 2 s)
-    ng = sorted((i for i, x in enumerate(plans) if x["family"] == "nestgen" and x["status"] == "OK"),
-                key=lambda i: -plans[i]["cfg"][0])
-    picks = pick(plans, "simt_affine", 6) + inlined[:4] + ng[:1]
+    # nest-generic candidates at this shape run the whole conv in <= 56
+    # interpreted threads (seconds each); their bit-exactness is covered on the
+    # ragged conv in test_gpu_e2e.py::test_ragged_shapes_every_candidate_exact
+    picks = pick(plans, "simt_affine", 6) + inlined[:4]
     assert len(pick(plans, "simt_affine", 6)) == 6 and len(inlined) >= 4
     if dtype == "bf16":
         tc = [i for i, x in enumerate(plans) if x["family"] == "tcgen05_conv"]
