@@ -28,7 +28,7 @@ using namespace lsb::tc;
   } while (0)
 
 struct P {
-  int N, K, BN, S, KT, CN, red, skip;
+  int N, K, BN, S, KT, CN, red, skip, ST;  // ST: ring stages (k-tiles in flight)
   float* c;
   float* ws;
   uint32_t* cnt;   // per tile arrival counter (never reset: epochs)
@@ -47,24 +47,28 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const int bbytes = p.BN * 128;
-  const uint32_t a0 = base, b0 = base + p.KT * kA;
-  const uint32_t ring = p.KT * (kA + bbytes);
+  const uint32_t a0 = base, b0 = base + p.ST * kA;
+  const uint32_t ring = p.ST * (kA + bbytes);
   const uint32_t stg = static_cast<uint32_t>(p.BN / 32) * 16384u;
   const uint32_t bars = base + (ring > stg ? ring : stg);
-  const uint32_t full = bars, done = bars + 8 * p.KT;
+  const uint32_t full = bars, empty = bars + 8 * p.ST, done = bars + 16 * p.ST;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(gbase + (done + 16 - base));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = blockIdx.x, split = blockIdx.z;
   const int tile = nb;
 
-  if (warp == 0) {
+  if (p.skip & 8) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (warp == 0 && !(p.skip & 4)) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                  "r"(p.tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (threadIdx.x == 32) {
-    for (int s = 0; s < p.KT; ++s) mbar_init(full + 8 * s, 1);
+  if (threadIdx.x == 32 && !(p.skip & 32)) {
+    for (int s = 0; s < p.ST; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 1);
+    }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
@@ -73,9 +77,9 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tslot;
+  const uint32_t tmem = (p.skip & 4) ? 0u : *tslot;
   if (p.CN > 1) cluster_arrive();
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!(p.skip & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (p.CN > 1) cluster_wait();
 
@@ -104,28 +108,33 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       const uint16_t mask = static_cast<uint16_t>((1u << p.CN) - 1u);
       for (int kt = 0; kt < p.KT; ++kt) {
         const int kc = (split * p.KT + kt) * 64;
-        mbar_expect_tx(full + 8 * kt, kA + bbytes);
+        const int s = kt % p.ST;
+        if (kt >= p.ST) mbar_wait(empty + 8 * s, ((kt / p.ST) & 1) ^ 1);
+        mbar_expect_tx(full + 8 * s, kA + bbytes);
         if (p.CN > 1)  // ta's box is {64, 128 / CN}: my row slice, into every CTA of the cluster
-          tma_load_3d_mc(a0 + kt * kA + rank * rows * 128, &ta, full + 8 * kt, kc, rank * rows, 0, mask);
+          tma_load_3d_mc(a0 + s * kA + rank * rows * 128, &ta, full + 8 * s, kc, rank * rows, 0, mask);
         else
-          tma_load_3d(a0 + kt * kA, &ta, full + 8 * kt, kc, 0, 0);
-        tma_load_3d(b0 + kt * bbytes, &tb, full + 8 * kt, kc, nb * p.BN, 0);
+          tma_load_3d(a0 + s * kA, &ta, full + 8 * s, kc, 0, 0);
+        tma_load_3d(b0 + s * bbytes, &tb, full + 8 * s, kc, nb * p.BN, 0);
       }
     } else if (warp == 1 && lane == 0) {
       for (int kt = 0; kt < p.KT; ++kt) {
-        mbar_wait(full + 8 * kt, 0);
+        const int s = kt % p.ST;
+        mbar_wait(full + 8 * s, (kt / p.ST) & 1);
         tc_fence_after();
-        const uint32_t sa = a0 + kt * kA, sb = b0 + kt * bbytes;
+        const uint32_t sa = a0 + s * kA, sb = b0 + s * bbytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), p.idesc, (kt | kk) != 0);
+        if (kt + p.ST < p.KT) umma_commit(empty + 8 * s);
       }
       umma_commit(done);
     }
-  } else if (threadIdx.x == 32) {
-    umma_commit(done);
+  } else if (threadIdx.x == 32 && !(p.skip & 32)) {
+    if (p.skip & 4) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(done) : "memory");
+    else umma_commit(done);
   }
-  mbar_wait(done, 0);
+  if (!(p.skip & 32)) mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
   if (p.skip & 2) goto out;
@@ -201,7 +210,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
 out:
   tc_fence_before();
   __syncthreads();
-  if (warp == 0)
+  if (warp == 0 && !(p.skip & 4))
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
 }
 
@@ -241,34 +250,36 @@ static uint16_t f2bf(float f) {
 
 int main(int argc, char** argv) {
   const int M = 128, N = 768, K = 3072;
-  struct V { int BN, S, CN, red, skip; };
+  struct V { int BN, S, CN, ST, skip; };  // ST 0: every k-tile in flight
   std::vector<V> vs;
-  const int bns[] = {32, 48, 64, 96, 128, 192, 256};
-  for (int bn : bns)
-    for (int S : {1, 2, 3, 4, 6, 8, 12, 16, 24, 48}) {
-      const int ctas = (N / bn) * S;
-      if (ctas < 48 || ctas > 296) continue;
-      for (int cn : {1, 2, 4})
-        for (int red : {0, 1}) {
-          if ((N / bn) % cn) continue;
-          if (S == 1 && red == 1) continue;
-          if (red == 1 && ctas > 148) continue;  // co-residency of a tile's splits (1 CTA/SM worst case)
-          vs.push_back({bn, S, cn, red, 0});
-        }
-    }
-  if (argc == 6) {  // one variant: BN S CN red skip
+  // launch-floor probes: 1|2 nothing, 4 no TMEM, 8 early launch_dependents, 16 no PDL, 32 no mbarriers
+  for (int S : {6, 12}) {
+    vs.push_back({32, S, 1, 0, 1 | 2 | 4 | 32});
+    vs.push_back({32, S, 1, 0, 1 | 2 | 4 | 32 | 8});
+    vs.push_back({32, S, 1, 0, 1 | 2 | 4 | 32 | 16});
+    vs.push_back({32, S, 1, 0, 1 | 2 | 4});
+    vs.push_back({32, S, 1, 0, 1 | 2});
+    vs.push_back({32, S, 1, 0, 1 | 2 | 8});
+    vs.push_back({32, S, 1, 0, 1 | 2 | 16});
+    vs.push_back({32, S, 1, 2, 1 | 2});
+    vs.push_back({32, S, 1, 2, 1 | 2 | 8});
+  }
+  vs.push_back({16, 12, 1, 0, 1 | 2 | 4 | 32});   // 576 CTAs
+  vs.push_back({64, 12, 1, 0, 1 | 2 | 4 | 32});   // 144 CTAs
+  vs.push_back({128, 12, 1, 0, 1 | 2 | 4 | 32});  // 72
+  // full kernels: stages and early trigger
+  for (int bn : {32, 64})
+    for (int S : {6, 12})
+      for (int st : {0, 1, 2})
+        for (int sk : {0, 8, 2, 10}) vs.push_back({bn, S, 1, st, sk});
+  if (argc == 6) {  // one variant: BN S CN ST skip
     vs.clear();
     vs.push_back({atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5])});
   }
   if (argc == 2) {  // list the default variants
-    for (const V& v : vs) printf("%d %d %d %d %d\n", v.BN, v.S, v.CN, v.red, v.skip);
+    for (const V& v : vs) printf("%d %d %d %d %d\n", v.BN, v.S, v.CN, v.ST, v.skip);
     return 0;
   }
-  // decomposition of the best-known config
-  vs.push_back({32, 12, 1, 0, 2});
-  vs.push_back({32, 12, 1, 0, 3});
-  vs.push_back({64, 12, 1, 0, 2});
-  vs.push_back({64, 12, 2, 0, 2});
   std::vector<uint16_t> ha(M * K), hb(N * K);
   std::vector<float> fa(M * K), fb(N * K);
   uint32_t s = 12345;
@@ -316,7 +327,7 @@ int main(int argc, char** argv) {
   void* scrub;
   CK(cudaMalloc(&scrub, 256 << 20));
 
-  if (argc != 6) printf("BN S CN red skip ctas smemKB | graph_us iso_us exact\n");
+  if (argc != 6) printf("BN S CN ST skip ctas smemKB | graph_us iso_us exact\n");
   for (const V& v : vs) {
     P p{};
     p.N = N;
@@ -325,7 +336,8 @@ int main(int argc, char** argv) {
     p.S = v.S;
     p.KT = K / 64 / v.S;
     p.CN = v.CN;
-    p.red = v.red;
+    p.red = 0;
+    p.ST = v.ST ? std::min(v.ST, p.KT) : p.KT;
     p.skip = v.skip;
     p.c = dc;
     p.ws = dws;
@@ -336,8 +348,8 @@ int main(int argc, char** argv) {
     uint32_t cols = 32;
     while (cols < static_cast<uint32_t>(v.BN)) cols <<= 1;
     p.tmem_cols = cols;
-    const int ring = p.KT * (kA + v.BN * 128), stgb = (v.BN / 32) * 16384;
-    const int smem = 1024 + std::max(ring, stgb) + 8 * p.KT + 32;
+    const int ring = p.ST * (kA + v.BN * 128), stgb = (v.BN / 32) * 16384;
+    const int smem = 1024 + std::max(ring, stgb) + 16 * p.ST + 32;
     if (smem > optin - 64) continue;
     CUtensorMap tmb = map3(db, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 1, 64, v.BN);
     CK(cudaMemsetAsync(dcnt, 0, 4096 * 4, st));
@@ -354,13 +366,13 @@ int main(int argc, char** argv) {
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    at[1].val.programmaticStreamSerializationAllowed = (v.skip & 16) ? 0 : 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
     const CUtensorMap tma = tma_cn[v.CN];
     auto launch = [&]() { return cudaLaunchKernelEx(&cfg, lab_kernel, tma, tmb, tmc, tmw, p); };
     if (launch() != cudaSuccess) {
-      printf("%d %d %d %d %d launch failed: %s\n", v.BN, v.S, v.CN, v.red, v.skip, cudaGetErrorString(cudaGetLastError()));
+      printf("%d %d %d %d %d launch failed: %s\n", v.BN, v.S, v.CN, v.ST, v.skip, cudaGetErrorString(cudaGetLastError()));
       continue;
     }
     CK(cudaStreamSynchronize(st));
@@ -400,8 +412,8 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(hc.data(), dc, M * N * 4, cudaMemcpyDeviceToHost));
     bool exact = true;
     for (int i = 0; i < M * N && exact; ++i) exact = static_cast<double>(hc[i]) == ref[i];
-    if (v.skip) exact = true;
-    printf("%3d %2d %d %d %d %3d %5.1f | %6.2f %6.2f %s\n", v.BN, v.S, v.CN, v.red, v.skip, (N / v.BN) * v.S,
+    if (v.skip & 3) exact = true;
+    printf("%3d %2d %d %d %2d %3d %5.1f | %6.2f %6.2f %s\n", v.BN, v.S, v.CN, p.ST, v.skip, (N / v.BN) * v.S,
            smem / 1024.0, best, iso[iso.size() / 2], exact ? "exact" : "MISMATCH");
     fflush(stdout);
     CK(cudaGraphExecDestroy(ge));
