@@ -14,6 +14,11 @@
  *     src/costmodel.py:21-79; looked up at src/search.py:141
  *   CostModel.predict_features(f) / _Validator._predict ls_score_batch
  *     src/costmodel.py:98-102; src/search.py:109-111
+ *   trace.validate_trace(e0, t) / replay(.., "follow") ls_replay_batch
+ *     src/trace.py:163-265 (+ ScheduleState, src/schedule.py:123-974);
+ *     called from _Validator.candidate, src/search.py:113-121
+ *   ir.structural_hash(p)                              ls_program_hash
+ *     src/ir.py:625-629
  *
  * Programs cross the boundary in the reference's own interchange format: the
  * text of `ir.serialize(program)` (`src/ir.py:708-715`).  The caller owns every
@@ -171,6 +176,37 @@ ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n);
 ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int launches, uint64_t* out,
                              int max_ctas, int* n_ctas);
 void ls_runner_destroy(ls_runner* r);
+
+/* ---- native trace replay / validation (host side, src/trace.py:163-265) ---
+ * A replayer holds one workload e0 (`ir.serialize` text).  ls_replay_batch
+ * replays each trace -- the text of the reference's `serialize_trace(t)`
+ * (src/trace.py:80-86), which _Validator already uses as its cache key -- with
+ * the recorded decisions, exactly as validate_trace does, and returns per trace:
+ *   ACCEPTED: program = ir.serialize(final program), hash = ir.structural_hash,
+ *             trace = serialize_trace(normalized trace)      (src/trace.py:196-198)
+ *   REJECTED: (reason, index) of the reference's Rejected verdict
+ *   DEFER:    the reference would raise something other than ReplayError on
+ *             this input (a malformed trace); the caller replays it with the
+ *             reference to get the reference's behaviour.
+ * Strings are malloc'd; release them with ls_replay_free. */
+enum { LS_REPLAY_ACCEPTED = 0, LS_REPLAY_REJECTED = 1, LS_REPLAY_DEFER = 2 };
+typedef struct {
+  int32_t status;
+  int32_t index;    /* REJECTED: instruction index (-1: workload hash mismatch) */
+  uint64_t hash;    /* ACCEPTED: structural hash of the final program */
+  char* program;
+  char* trace;
+  char* reason;
+} ls_replay_result;
+typedef struct ls_replayer ls_replayer;
+ls_status ls_replayer_create(const char* e0, size_t len, ls_replayer** out);
+ls_status ls_replayer_hash(ls_replayer* r, uint64_t* out); /* ir.structural_hash(e0) */
+ls_status ls_replay_batch(ls_replayer* r, const char* const* traces, const size_t* lens, int n,
+                          ls_replay_result* out);
+void ls_replay_free(ls_replay_result* res, int n);
+void ls_replayer_destroy(ls_replayer* r);
+/* ir.structural_hash of a serialized program */
+ls_status ls_program_hash(const char* program, size_t len, uint64_t* out);
 
 const char* ls_last_error(void);
 const char* ls_version(void);

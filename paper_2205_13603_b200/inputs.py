@@ -26,6 +26,9 @@ def program_text(p) -> str:
     prog = getattr(p, "program", p)  # a search Candidate / TuningRecord-like object
     if isinstance(prog, str):
         return prog
+    text = getattr(prog, "_ls_text", None)  # replay.LazyProgram: the native replay's own text
+    if text is not None:
+        return text
     return loopsched().ir.serialize(prog)
 
 

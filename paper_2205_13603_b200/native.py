@@ -54,6 +54,11 @@ class ResultC(ctypes.Structure):
                 ("mismatches", ctypes.c_int64), ("checked_ns", ctypes.c_double)]
 
 
+class ReplayResultC(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("index", ctypes.c_int32), ("hash", ctypes.c_uint64),
+                ("program", ctypes.c_void_p), ("trace", ctypes.c_void_p), ("reason", ctypes.c_void_p)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "ls_sim_latency_batch": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p),
@@ -99,6 +104,14 @@ EXPORTS = {
     "ls_runner_trace_tc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, c_i32p]),
     "ls_runner_destroy": (None, [ctypes.c_void_p]),
+    "ls_replayer_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "ls_replayer_hash": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]),
+    "ls_replay_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                       ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                       ctypes.POINTER(ReplayResultC)]),
+    "ls_replay_free": (None, [ctypes.POINTER(ReplayResultC), ctypes.c_int]),
+    "ls_replayer_destroy": (None, [ctypes.c_void_p]),
+    "ls_program_hash": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64)]),
     "ls_last_error": (ctypes.c_char_p, []),
     "ls_version": (ctypes.c_char_p, []),
 }

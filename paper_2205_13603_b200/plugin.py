@@ -15,6 +15,8 @@ The reference's search driver (`tune` / `evolve` / `mutate` / `mh_accept`,
   ``_Validator._predict`` (:109-111; the  K7b: every known feature row rescored in
   reference's own plug-in seam,           one launch per model, then lookups
   tests/test_search.py:125-127)
+  ``search._Validator`` (:100-146,        ``replay.NativeValidator``: validate_trace
+  constructed at :324 and :169)           replayed natively (``ls_replay_batch``)
   ======================================  ===========================================
 
 Nothing in the reference is edited or copied; the originals are restored on
@@ -119,9 +121,10 @@ def positive_score(s: float) -> float:
 class _Seams:
     """What one ``installed()`` block routes the reference's seams to."""
 
-    def __init__(self, runner, cache):
+    def __init__(self, runner, cache, native_replay=True):
         self.runner = runner
         self.cache = cache
+        self.native_replay = native_replay
 
 
 _tls = threading.local()
@@ -156,6 +159,16 @@ def _d_featurize(p, spec=None):
     return _originals[2](p, spec) if spec is not None else _originals[2](p)
 
 
+def _d_validator(e0, machine_spec=None):
+    cur = _current()
+    base = _originals[4]
+    if cur is not None and cur.native_replay:
+        from .replay import native_validator_class
+        cls = native_validator_class()
+        return cls(e0, machine_spec) if machine_spec is not None else cls(e0)
+    return base(e0, machine_spec) if machine_spec is not None else base(e0)
+
+
 def _d_predict(self, program, features, model):
     cur = _current()
     if cur is not None and cur.cache is not None:
@@ -164,7 +177,7 @@ def _d_predict(self, program, features, model):
 
 
 @contextlib.contextmanager
-def installed(runner=None, scorer=None, exact_scores: bool = False):
+def installed(runner=None, scorer=None, exact_scores: bool = False, native_replay: bool = True):
     """Route the reference's seams to ``runner`` (Runner protocol) and
     ``scorer`` (Scorer protocol) inside the block.
 
@@ -172,21 +185,26 @@ def installed(runner=None, scorer=None, exact_scores: bool = False):
     innermost ``installed()`` block of the CALLING THREAD (falling back to the
     reference's originals), so concurrent tunes on several threads -- e.g. one
     per GPU -- each see their own runner; the originals are restored when the
-    last block exits, also when the search raises."""
+    last block exits, also when the search raises.  ``native_replay``
+    routes ``validate_trace`` through the native replay (replay.py)."""
     global _install_depth, _originals
     ls = loopsched()
     S = ls.search
     cache = ScoreCache(scorer, exact=exact_scores) if scorer is not None else None
     with _install_lock:
         if _install_depth == 0:
-            _originals = (S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict)
+            vcls = S._Validator
+            _originals = (S._measure_batch, S.simulate_latency, S.featurize, vcls._predict, vcls)
             S._measure_batch, S.simulate_latency, S.featurize = _d_measure, _d_simulate, _d_featurize
-            S._Validator._predict = _d_predict
+            vcls._predict = _d_predict
+            _d_validator._ls_dispatch = True
+            _d_validator._ls_base = vcls
+            S._Validator = _d_validator
         _install_depth += 1
     st = getattr(_tls, "stack", None)
     if st is None:
         st = _tls.stack = []
-    st.append(_Seams(runner, cache))
+    st.append(_Seams(runner, cache, native_replay))
     try:
         yield cache
     finally:
@@ -194,7 +212,9 @@ def installed(runner=None, scorer=None, exact_scores: bool = False):
         with _install_lock:
             _install_depth -= 1
             if _install_depth == 0:
-                S._measure_batch, S.simulate_latency, S.featurize, S._Validator._predict = _originals
+                vcls = _originals[4]
+                S._measure_batch, S.simulate_latency, S.featurize, vcls._predict = _originals[:4]
+                S._Validator = vcls
                 _originals = None
 
 
