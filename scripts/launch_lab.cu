@@ -22,7 +22,10 @@
 
 // flags: 1 griddepcontrol (trigger at entry + wait), 2 TMEM alloc/dealloc,
 // 4 touch the dynamic smem (one store per thread), 8 trigger after the TMEM alloc
-__global__ void __launch_bounds__(256, 1) probe(int flags, int* sink) {
+struct Big {
+  uint8_t b[640];
+};
+__global__ void __launch_bounds__(256, 1) probe(int flags, int* sink, const __grid_constant__ Big big) {
   extern __shared__ uint8_t sm[];
   __shared__ uint32_t slot;
   if ((flags & 1) && !(flags & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -40,7 +43,7 @@ __global__ void __launch_bounds__(256, 1) probe(int flags, int* sink) {
   if ((flags & 1) && (flags & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (flags & 1) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (flags & 4) sm[threadIdx.x * 4] = static_cast<uint8_t>(threadIdx.x);
-  if (threadIdx.x == 0 && blockIdx.x == 0 && flags < 0) *sink = sm[0];
+  if (threadIdx.x == 0 && blockIdx.x == 0 && flags < 0) *sink = sm[0] + big.b[threadIdx.x];
   if (flags & 2) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -50,7 +53,7 @@ __global__ void __launch_bounds__(256, 1) probe(int flags, int* sink) {
 }
 
 struct Cfg {
-  int grid, threads, smem_kb, flags, pdl;
+  int grid, threads, smem_kb, flags, pdl, cluster = 0;
 };
 
 int main() {
@@ -70,6 +73,7 @@ int main() {
       {144, 128, 161, 0, 0},  {144, 128, 161, 11, 1}, {288, 128, 81, 1, 1},   {288, 128, 81, 3, 1},
       {288, 128, 81, 0, 0},   {288, 128, 0, 1, 1},    {288, 128, 0, 3, 1},    {148, 128, 161, 3, 1},
       {144, 256, 161, 3, 1},  {72, 128, 161, 3, 1},   {576, 128, 40, 3, 1},   {144, 128, 161, 7, 1},
+      {144, 128, 161, 3, 1, 1}, {288, 128, 81, 3, 1, 1}, {144, 128, 161, 3, 1, 2}, {144, 128, 0, 1, 1, 1},
   };
   const int G = 64, R = 7;
   std::vector<std::vector<float>> t(cs.size());
@@ -81,14 +85,19 @@ int main() {
     cfg.blockDim = dim3(c.threads);
     cfg.dynamicSmemBytes = static_cast<size_t>(c.smem_kb) * 1024;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = c.pdl;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = c.cluster ? c.cluster : 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = c.cluster ? 2 : 1;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < G; ++k) CK(cudaLaunchKernelEx(&cfg, probe, c.flags, sink));
+    Big big{};
+    for (int k = 0; k < G; ++k) CK(cudaLaunchKernelEx(&cfg, probe, c.flags, sink, big));
     CK(cudaStreamEndCapture(st, &g));
     CK(cudaGraphInstantiate(&ge[i], g, 0));
     CK(cudaGraphLaunch(ge[i], st));
@@ -105,10 +114,11 @@ int main() {
       CK(cudaEventElapsedTime(&ms, e0, e1));
       t[i].push_back(ms * 1000.f / G);
     }
-  printf("grid threads smemKB flags pdl | median_us min_us\n");
+  printf("grid threads smemKB flags pdl cluster | median_us min_us   (640-byte __grid_constant__ param)\n");
   for (size_t i = 0; i < cs.size(); ++i) {
     std::sort(t[i].begin(), t[i].end());
-    printf("%4d %4d %4d %3d %d | %6.3f %6.3f\n", cs[i].grid, cs[i].threads, cs[i].smem_kb, cs[i].flags, cs[i].pdl,
+    printf("%4d %4d %4d %3d %d %d | %6.3f %6.3f\n", cs[i].grid, cs[i].threads, cs[i].smem_kb, cs[i].flags, cs[i].pdl,
+           cs[i].cluster,
            t[i][R / 2], t[i][0]);
   }
   return 0;
