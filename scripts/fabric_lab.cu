@@ -30,6 +30,11 @@ struct P {
   int shared;   // of which the first `shared` are the same for every CTA (an A operand)
   int nred;     // 16 KB fp32 boxes add-reduced per CTA
   int share;    // CTAs adding into the same C region (split-K ways)
+  int how;      // 0 TMA tensor add-reduce, 1 TMA tensor store, 2 red.global.add.v4.f32,
+                // 3 st.global.v4, 4 bulk (1-D) add-reduce, 5 TMA add-reduce without the write wait,
+                // 6 DSMEM reduce-scatter inside a cluster of `share` CTAs (bulk copies of 16 KB / share
+                //   per peer per box), then each CTA TMA-add-reduces its 1/share slice
+  float* c;     // the fp32 region buffer (generic-proxy variants)
 };
 
 __global__ void __launch_bounds__(128, 1) fabric(const __grid_constant__ CUtensorMap tl,
@@ -37,13 +42,17 @@ __global__ void __launch_bounds__(128, 1) fabric(const __grid_constant__ CUtenso
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
-  __shared__ alignas(8) uint64_t bar;
-  const uint32_t b = smem_u32(&bar);
+  __shared__ alignas(8) uint64_t bar, rbar;
+  const uint32_t b = smem_u32(&bar), rb = smem_u32(&rbar);
+  const uint32_t recv = base + 4 * 16384;  // receive area after the staged boxes
   if (threadIdx.x == 0) {
     mbar_init(b, 1);
+    mbar_init(rb, 1);
+    if (p.how == 6) mbar_expect_tx(rb, static_cast<uint32_t>(p.nred * (p.share - 1) * (16384 / p.share)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (p.how == 6) cluster_sync_all();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0 && p.nld > 0) {
@@ -58,11 +67,60 @@ __global__ void __launch_bounds__(128, 1) fabric(const __grid_constant__ CUtenso
     // smem already holds bytes (whatever was loaded / garbage): reduce them
     fence_proxy_async_smem();
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const int region = blockIdx.x / p.share;
-      for (int i = 0; i < p.nred; ++i) tma_reduce_add_3d(&tr, base + i * 16384, 0, (region * p.nred + i) * 128, 0);
-      bulk_commit();
-      bulk_wait_all();
+    const int region = blockIdx.x / p.share;
+    if (p.how == 0 || p.how == 1 || p.how == 5) {
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < p.nred; ++i) {
+          if (p.how == 1) tma_store_3d(&tr, base + i * 16384, 0, (region * p.nred + i) * 128, 0);
+          else tma_reduce_add_3d(&tr, base + i * 16384, 0, (region * p.nred + i) * 128, 0);
+        }
+        bulk_commit();
+        if (p.how == 5) bulk_wait_read();
+        else bulk_wait_all();
+      }
+    } else if (p.how == 6) {
+      const uint32_t me = cluster_rank();
+      const uint32_t slice = 16384u / static_cast<uint32_t>(p.share);
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < p.nred; ++i)
+          for (int o = 0; o < p.share; ++o) {
+            if (o == static_cast<int>(me)) continue;
+            const uint32_t src = base + i * 16384 + o * slice;
+            const uint32_t dst = map_peer(recv + (i * p.share + me) * slice, o);
+            bulk_push_peer(dst, src, slice, map_peer(rb, o));
+          }
+      }
+      mbar_wait(rb, 0);
+      // (the sum of the received slices into my slice is ALU work, omitted)
+      if (threadIdx.x == 0) {
+        const int region = blockIdx.x / p.share;
+        for (int i = 0; i < p.nred; ++i)
+          tma_reduce_add_3d(&tr, base + i * 16384 + me * slice, 0, (region * p.nred + i) * 128 + me * (128 / p.share), 0);
+        bulk_commit();
+        bulk_wait_all();
+      }
+      cluster_sync_all();  // no peer may still push into me when I exit
+    } else if (p.how == 4) {
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < p.nred; ++i) {
+          float* dst = p.c + static_cast<int64_t>(region * p.nred + i) * 4096;
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 16384;" ::"l"(dst),
+                       "r"(base + i * 16384)
+                       : "memory");
+        }
+        bulk_commit();
+        bulk_wait_all();
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(smem_raw + (base - raw));
+      for (int i = 0; i < p.nred; ++i) {
+        float4* dst = reinterpret_cast<float4*>(p.c + static_cast<int64_t>(region * p.nred + i) * 4096);
+        for (int e = threadIdx.x; e < 1024; e += 128) {
+          const float4 v = src[i * 1024 + e];
+          if (p.how == 2) red_add_f4(reinterpret_cast<float*>(dst + e), v);
+          else dst[e] = v;
+        }
+      }
     }
   }
   __syncthreads();
@@ -117,13 +175,18 @@ int main() {
   for (int g : {144, 288})
     for (int nld : {0, 2, 4, 6, 8}) {
       if (g == 288 && nld > 6) continue;
-      cs.push_back({g, {nld, 0, 0, 1}});
-      if (nld >= 4) cs.push_back({g, {nld, nld / 2, 0, 1}});
-      if (nld >= 2) cs.push_back({g, {nld, nld, 0, 1}});
+      cs.push_back({g, {nld, 0, 0, 1, 0, nullptr}});
+      if (nld >= 4) cs.push_back({g, {nld, nld / 2, 0, 1, 0, nullptr}});
+      if (nld >= 2) cs.push_back({g, {nld, nld, 0, 1, 0, nullptr}});
     }
   for (int g : {144, 288})
-    for (int nred : {1, 2, 4})
-      for (int share : {1, 6, 12, 24}) cs.push_back({g, {0, 0, nred, share}});
+    for (int nred : {1, 2})
+      for (int how : {0, 1, 6})
+        for (int share : {1, 2, 4}) {
+          if (how == 6 && share == 1) continue;
+          if (how != 6 && share != 1) continue;
+          cs.push_back({g, {0, 0, nred, share, how, reinterpret_cast<float*>(dr)}});
+        }
   // BERT-FFN shapes: BN 32 / S 12 (288 CTAs: 4 k-tiles of A 16K (shared by 24 N-tiles) + B 4K)
   const int G = 64, R = 7;
   std::vector<std::vector<float>> t(cs.size());
@@ -133,13 +196,17 @@ int main() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs[i].grid);
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = 1024 + nbox * 16384;
+    cfg.dynamicSmemBytes = 1024 + 4 * 16384 + nbox * 16384;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cs[i].p.how == 6 ? cs[i].p.share : 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cs[i].p.how == 6 ? 2 : 1;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < G; ++k) CK(cudaLaunchKernelEx(&cfg, fabric, tl, tr, cs[i].p));
@@ -159,11 +226,11 @@ int main() {
       CK(cudaEventElapsedTime(&ms, e0, e1));
       t[i].push_back(ms * 1000.f / G);
     }
-  printf("grid nld shared nred share | median_us  loadMB redMB\n");
+  printf("grid nld shared nred share how | median_us  loadMB redMB\n");
   for (size_t i = 0; i < cs.size(); ++i) {
     std::sort(t[i].begin(), t[i].end());
     const P& p = cs[i].p;
-    printf("%4d %2d %2d %2d %2d | %6.3f  %6.2f %6.2f\n", cs[i].grid, p.nld, p.shared, p.nred, p.share, t[i][R / 2],
+    printf("%4d %2d %2d %2d %2d %d | %6.3f  %6.2f %6.2f\n", cs[i].grid, p.nld, p.shared, p.nred, p.share, p.how, t[i][R / 2],
            cs[i].grid * p.nld * 16384 / 1e6, cs[i].grid * p.nred * 16384 / 1e6);
   }
   return 0;

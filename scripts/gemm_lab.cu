@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "../paper_2205_13603_b200/csrc/tc_common.cuh"
@@ -29,6 +30,7 @@ using namespace lsb::tc;
 
 struct P {
   int N, K, BN, S, KT, CN, red, skip, ST;  // ST: ring stages (k-tiles in flight)
+  unsigned long long* tr;  // optional per-CTA %globaltimer stamps (9 per CTA)
   float* c;
   float* ws;
   uint32_t* cnt;   // per tile arrival counter (never reset: epochs)
@@ -56,6 +58,13 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = blockIdx.x, split = blockIdx.z;
   const int tile = nb;
+  unsigned long long* tr = p.tr ? p.tr + 9 * (blockIdx.z * gridDim.x + blockIdx.x) : nullptr;
+  if (tr && threadIdx.x == 0) {
+    tr[0] = gtime();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[8] = smid;
+  }
 
   if (p.skip & 8) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0 && !(p.skip & 4)) {
@@ -80,7 +89,9 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   const uint32_t tmem = (p.skip & 4) ? 0u : *tslot;
   if (p.CN > 1) cluster_arrive();
   if (!(p.skip & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tr && threadIdx.x == 0) tr[2] = gtime();
   if (p.CN > 1) cluster_wait();
 
   float* ctile = p.c + static_cast<int64_t>(nb) * p.BN;
@@ -122,6 +133,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         const int s = kt % p.ST;
         mbar_wait(full + 8 * s, (kt / p.ST) & 1);
         tc_fence_after();
+        if (tr && kt == 0) tr[3] = gtime();
         const uint32_t sa = a0 + s * kA, sb = b0 + s * bbytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -137,6 +149,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   if (!(p.skip & 32)) mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
+  if (tr && threadIdx.x == 0) tr[4] = gtime();
   if (p.skip & 2) goto out;
   {
     const int row = warp * 32 + lane;
@@ -155,6 +168,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     }
     fence_proxy_async_smem();
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[5] = gtime();
     if (p.S == 1) {
       if (threadIdx.x == 0) {
         for (int c0 = 0; c0 < p.BN; c0 += 32) tma_store_3d(&tc, base + (c0 / 32) * 16384, nb * p.BN + c0, 0, 0);
@@ -169,10 +183,12 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         __syncthreads();
       }
       if (threadIdx.x == 0) {
+        if (tr) tr[6] = gtime();
         fence_proxy_async_global();
         for (int c0 = 0; c0 < p.BN; c0 += 32) tma_reduce_add_3d(&tc, base + (c0 / 32) * 16384, nb * p.BN + c0, 0, 0);
         bulk_commit();
         bulk_wait_all();
+        if (tr) tr[7] = gtime();
       }
     } else {
       // fixed-order reduction: partial -> ws[split]; arrive; every CTA of the
@@ -272,7 +288,8 @@ int main(int argc, char** argv) {
     for (int S : {6, 12})
       for (int st : {0, 1, 2})
         for (int sk : {0, 8, 2, 10}) vs.push_back({bn, S, 1, st, sk});
-  if (argc == 6) {  // one variant: BN S CN ST skip
+  const bool trace = argc == 7 && std::string(argv[6]) == "trace";
+  if (argc == 6 || trace) {  // one variant: BN S CN ST skip [trace]
     vs.clear();
     vs.push_back({atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5])});
   }
@@ -327,7 +344,7 @@ int main(int argc, char** argv) {
   void* scrub;
   CK(cudaMalloc(&scrub, 256 << 20));
 
-  if (argc != 6) printf("BN S CN ST skip ctas smemKB | graph_us iso_us exact\n");
+  if (argc != 6 && !trace) printf("BN S CN ST skip ctas smemKB | graph_us iso_us exact\n");
   for (const V& v : vs) {
     P p{};
     p.N = N;
@@ -378,23 +395,71 @@ int main(int argc, char** argv) {
     CK(cudaStreamSynchronize(st));
     // graph of G back-to-back launches
     const int G = 64;
+    const int ctas = (N / v.BN) * v.S;
+    unsigned long long* dtr = nullptr;
+    if (trace) {
+      CK(cudaMalloc(&dtr, sizeof(unsigned long long) * G * ctas * 9));
+      CK(cudaMemset(dtr, 0, sizeof(unsigned long long) * G * ctas * 9));
+    }
     cudaGraph_t g;
     cudaGraphExec_t ge;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < G; ++i) CK(launch());
+    for (int i = 0; i < G; ++i) {
+      p.tr = trace ? dtr + static_cast<size_t>(i) * ctas * 9 : nullptr;
+      CK(launch());
+    }
+    p.tr = nullptr;
     CK(cudaStreamEndCapture(st, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
     CK(cudaStreamSynchronize(st));
     float best = 1e30f;
-    for (int rep = 0; rep < 5; ++rep) {
+    std::vector<float> gt;
+    for (int rep = 0; rep < 7; ++rep) {
+      CK(cudaGraphLaunch(ge, st));  // keep the clocks up: the timed replay follows a busy GPU
       CK(cudaEventRecord(e0, st));
       CK(cudaGraphLaunch(ge, st));
       CK(cudaEventRecord(e1, st));
       CK(cudaEventSynchronize(e1));
       float ms;
       CK(cudaEventElapsedTime(&ms, e0, e1));
-      best = std::min(best, ms * 1000.f / G);
+      gt.push_back(ms * 1000.f / G);
+    }
+    std::sort(gt.begin(), gt.end());
+    best = gt[gt.size() / 2];  // median
+    if (trace) {
+      std::vector<unsigned long long> h(static_cast<size_t>(G) * ctas * 9);
+      CK(cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost));
+      const char* names[8] = {"entry", "setup", "depwait", "1st k-tile", "mma done", "staged", "flag", "reduced"};
+      std::vector<std::vector<double>> ph(8);
+      std::vector<double> gap, span, skew;
+      for (int L = 8; L < G; ++L) {
+        const unsigned long long* a = &h[static_cast<size_t>(L) * ctas * 9];
+        const unsigned long long* b = &h[static_cast<size_t>(L - 1) * ctas * 9];
+        unsigned long long t0min = ~0ull, t0max = 0, endmax = 0, pend = 0;
+        for (int c = 0; c < ctas; ++c) {
+          t0min = std::min(t0min, a[9 * c]);
+          t0max = std::max(t0max, a[9 * c]);
+          for (int k = 0; k < 8; ++k) if (a[9 * c + k]) endmax = std::max(endmax, a[9 * c + k]);
+          for (int k = 0; k < 8; ++k) if (b[9 * c + k]) pend = std::max(pend, b[9 * c + k]);
+        }
+        gap.push_back(static_cast<double>(t0min) - static_cast<double>(pend));
+        span.push_back(static_cast<double>(endmax - t0min));
+        skew.push_back(static_cast<double>(t0max - t0min));
+        for (int c = 0; c < ctas; ++c)
+          for (int k = 1; k < 8; ++k) {
+            const unsigned long long x = a[9 * c + k], y = a[9 * c + k - 1];
+            if (x && y) ph[k].push_back(static_cast<double>(x) - static_cast<double>(y));
+          }
+      }
+      auto med = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+      auto p90 = [](std::vector<double> v) { if (v.empty()) return 0.0; std::sort(v.begin(), v.end()); return v[v.size() * 9 / 10]; };
+      printf("trace BN %d S %d CN %d ST %d: per-launch %.2f us; span(first entry->last stamp) med %.0f ns, "
+             "start skew med %.0f ns, gap(prev last stamp->first entry) med %.0f ns\n",
+             v.BN, v.S, v.CN, p.ST, best, med(span), med(skew), med(gap));
+      for (int k = 1; k < 8; ++k)
+        printf("  %-10s -> %-10s  med %6.0f ns  p90 %6.0f ns\n", names[k - 1], names[k], med(ph[k]), p90(ph[k]));
+      CK(cudaFree(dtr));
     }
     // isolated: L2 warm, one launch between events
     std::vector<float> iso;
