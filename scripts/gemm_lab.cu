@@ -45,6 +45,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
            const __grid_constant__ CUtensorMap tc, const __grid_constant__ CUtensorMap tw, P p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
+  __shared__ volatile uint32_t s_ready;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -73,6 +74,7 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (threadIdx.x == 0) s_ready = 0;
   if (threadIdx.x == 32 && !(p.skip & 32)) {
     for (int s = 0; s < p.ST; ++s) {
       mbar_init(full + 8 * s, 1);
@@ -120,6 +122,10 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       }
       asm volatile("bar.sync 1, 64;" ::: "memory");
       if (t2 == 0) st_release_u32(p.flag + tile, t / p.S + 1);
+    } else if ((p.skip & 512) && t2 == 0) {
+      // skip 512: observe the tile's zeroing while the operands stream in
+      while (ld_acquire_u32(p.flag + tile) < t / p.S + 1) __nanosleep(32);
+      s_ready = 1;
     }
   }
 
@@ -216,9 +222,15 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
       }
     } else if (p.red == 0) {
       if (s_ticket % static_cast<uint32_t>(p.S) != 0) {
-        if (threadIdx.x == 0)
-          while (ld_acquire_u32(p.flag + tile) < s_ticket / static_cast<uint32_t>(p.S) + 1) {
+        if (threadIdx.x == 0) {
+          if (p.skip & 512) {
+            while (!s_ready) {
+            }
+          } else {
+            while (ld_acquire_u32(p.flag + tile) < s_ticket / static_cast<uint32_t>(p.S) + 1) {
+            }
           }
+        }
         __syncthreads();
       }
       if (threadIdx.x == 0) {
@@ -226,7 +238,8 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
         fence_proxy_async_global();
         for (int c0 = 0; c0 < p.BN; c0 += 32) tma_reduce_add_3d(&tc, base + (c0 / 32) * 16384, nb * p.BN + c0, 0, 0);
         bulk_commit();
-        bulk_wait_all();
+        if (p.skip & 1024) bulk_wait_read();
+        else bulk_wait_all();
         if (tr) tr[7] = gtime();
       }
     } else {
