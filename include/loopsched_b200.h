@@ -172,7 +172,8 @@ ls_status ls_runner_launch_count(ls_runner* r, int64_t* count);
 ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n);
 /* Diagnostics: launch one tcgen05 candidate `launches` times back to back with
  * per-CTA %globaltimer stamps (8 u64 per CTA: start, setup done, first stage
- * landed, accumulator done, partial tile staged, stored, smid, 0). */
+ * landed, accumulator done, partial tile staged, zeroing flag acquired,
+ * stored, smid). */
 ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int launches, uint64_t* out,
                              int max_ctas, int* n_ctas);
 void ls_runner_destroy(ls_runner* r);

@@ -68,7 +68,6 @@ struct TcLaunch {
   int m, n, k;
   int bn, splits, kt, stages, batch, grid_m, grid_n;
   int smem_bytes;
-  bool direct = false;                  // TcGeom::direct (from the plan)
   unsigned long long* trace = nullptr;  // optional per-CTA timeline (8 stamps per CTA)
   uint32_t* sync = nullptr;             // split-K ticket slots of this candidate (2 x kTcSyncSlots, zeroed)
   bool pdl = true;                      // programmatic dependent launch

@@ -238,16 +238,13 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
         if (before_spatial) t.splits *= merged[i].extent;
         else t.kt *= merged[i].extent;
       }
-      // stage count: as many k-tiles as fit beside the reduction buffer (<= 8)
+      // stage count: as many k-tiles as fit in shared memory (<= 8)
       const int64_t tiles = t.batch * t.grid_m * t.grid_n;
-      TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles, t.grid_n, lim.max_smem);
-      int64_t avail = lim.max_smem - 1024 - 256 - g0.recv;
-      t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / g0.stage_bytes));
-      static const int64_t max_stages = getenv("LSB_TC_MAXSTAGES") ? atoi(getenv("LSB_TC_MAXSTAGES")) : 8;
-      t.stages = std::min<int64_t>(t.stages, std::max<int64_t>(1, max_stages));
-      TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles, t.grid_n, lim.max_smem);
+      const TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles);
+      const int64_t avail = lim.max_smem - 1024 - 256;
+      t.stages = std::min<int64_t>({t.kt, std::max<int64_t>(1, avail / g0.stage_bytes), 8});
+      const TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles);
       plan.needs_zero = g.mode == 3;
-      t.direct = g.direct;
       t.smem_bytes = g.smem;
       int32_t* c = plan.cfg;
       c[0] = static_cast<int32_t>(t.batch); c[1] = static_cast<int32_t>(t.grid_m);

@@ -70,66 +70,40 @@ struct SimtCfg {
 struct TcCfg {
   int64_t bn, splits, kt, grid_m, grid_n, batch;
   int64_t stages, smem_bytes;
-  bool direct;  // TcGeom::direct under the planning device's smem limit
 };
 
 // Split-K reduction of the TCGEN05 family and the shared-memory layout it
 // implies (tc_gemm.cu).
 //   mode 0: splits == 1   single CTA per tile, plain stores
-//   mode 1: cluster       the splits CTAs of a tile form one cluster (<= 16)
-//                         and reduce-scatter their fp32 partials through
-//                         distributed shared memory (bulk DSMEM copies)
 //   mode 2: L2 reduction  the first CTA of the tile to start zeroes it (its
 //                         loads are in flight), every split adds its partial
 //                         (TMA add-reduce) once the zeroing is released; the
 //                         arrival ticket per tile also gives each launch its
 //                         own epoch, so there is no memset node between
 //                         launches
-//   mode 3: mode 2 without ticket slots: fp32 atomics into a memset C
-// DSMEM moves ~20 B/clk per SM (B300_MICROARCH.md), below the SM's L2 red
-// bandwidth, so mode 2 is the default; mode 1 stays for experiments.
+//   mode 3: mode 2 beyond kTcSyncSlots tiles: fp32 atomics into a memset C
+// Measured and dropped (profiles/r01b_summary.md §1, profiles/r02_gemm_lab.md):
+// cluster reduce-scatter through DSMEM (~20 B/clk per SM, below the L2 add
+// rate), TMA multicast of A across N-tiles (L2 already dedups concurrent
+// reads), a store-first epilogue without zeroing, early zero-flag polling.
 constexpr int kTcSyncSlots = 4096;  // ticket slots per candidate (mode 2)
 struct TcGeom {
-  int mode = 0, cl = 1, parts = 1, rows_per = 128, ld = 0;
-  int mc = 1;               // N-tiles per cluster sharing each A k-tile by TMA multicast
-  bool direct = false;      // tile + receive buffer do not fit: push rows straight from registers
+  int mode = 0;
+  bool tma_epi = false;     // BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
+  int ld = 0;               // padded fp32 row of the staged tile (generic epilogue)
   int64_t stage_bytes = 0;  // one k-tile: A 128x64 + B BNx64 bf16
-  int64_t ring = 0, tile = 0, recv = 0, smem = 0;
+  int64_t ring = 0, tile = 0, smem = 0;
 };
-inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles, int64_t grid_n,
-                      int64_t max_smem = 227 * 1024) {
+inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles) {
   TcGeom g;
+  g.mode = splits == 1 ? 0 : tiles <= kTcSyncSlots ? 2 : 3;
+  g.tma_epi = bn % 32 == 0 && g.mode != 3;
   g.ld = static_cast<int>(bn + 4);  // padded fp32 row (16-byte aligned, conflict-free)
-  // experiment knobs (scripts/tc_sweep.py): LSB_TC_MAXCL1 = largest split
-  // reduced in one cluster (mode 1, default 0 = never), LSB_TC_ATOMIC=1 =
-  // memset + atomics instead of mode 2
-  static const int maxcl1 = getenv("LSB_TC_MAXCL1") ? atoi(getenv("LSB_TC_MAXCL1")) : 0;
-  static const bool atomic = getenv("LSB_TC_ATOMIC") && atoi(getenv("LSB_TC_ATOMIC")) != 0;
-  if (splits == 1) {
-    g.mode = 0;
-  } else if (splits <= maxcl1 && splits <= 16) {
-    g.mode = 1;
-    g.cl = static_cast<int>(splits);
-  } else {
-    g.mode = tiles <= kTcSyncSlots && !atomic ? 2 : 3;
-    g.parts = static_cast<int>(splits);
-  }
-  // A multicast: the N-tiles of one (batch, m, split) read the same A k-tile;
-  // a cluster of mc of them along N loads it once (each CTA one 128/mc-row
-  // slice, multicast to all).  Measured slower on the BERT shapes (L2 already
-  // dedups concurrent unicast reads; clusters of 8 spread CTA start times by
-  // several us), so off by default: LSB_TC_MC=2|4|8 enables it.
-  static const int mc_cap = getenv("LSB_TC_MC") ? atoi(getenv("LSB_TC_MC")) : 1;
-  if (g.mode != 1)
-    for (int m = std::min(mc_cap, 8); m >= 2; m /= 2)
-      if (grid_n % m == 0) { g.mc = m; break; }
-  g.rows_per = (128 + g.cl - 1) / g.cl;
   g.stage_bytes = 128 * 64 * 2 + bn * 64 * 2;
   g.ring = stages * g.stage_bytes;
-  g.tile = 128LL * g.ld * 4;  // staged accumulator tile, overlays the finished ring
-  g.recv = g.cl > 1 ? static_cast<int64_t>(g.cl) * g.rows_per * g.ld * 4 : 0;
-  g.direct = g.cl > 1 && 1024 + std::max(g.stage_bytes, g.tile) + g.recv + 256 > max_smem;
-  g.smem = 1024 + (g.direct ? g.ring : std::max(g.ring, g.tile)) + g.recv + 256;
+  // staged accumulator tile, overlays the finished ring
+  g.tile = g.tma_epi ? (bn / 32) * 16384 : 128LL * g.ld * 4;
+  g.smem = 1024 + std::max(g.ring, g.tile) + 256;
   return g;
 }
 

@@ -62,16 +62,6 @@ EncodeTiledFn encode_fn() {
 }
 
 // bf16 K-major operand [batch][rows][K] as a 3-D TMA map with a {64, box_rows, 1} box.
-CUtensorMapL2promotion l2_promo() {  // experiment knob LSB_TMA_PROMO: 0 none, 1 64B, 2 128B, 3 256B (default)
-  static const int v = getenv("LSB_TMA_PROMO") ? atoi(getenv("LSB_TMA_PROMO")) : 3;
-  switch (v) {
-    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
-    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  }
-}
-
 bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, int64_t k, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
@@ -80,7 +70,7 @@ bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, 
   cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -312,7 +302,7 @@ struct ls_runner {
         if (!want) continue;
       } else {
         if (p.family != F_TC) continue;
-        if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n, p.tc.grid_n).mode != 2)
+        if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n).mode != 2)
           continue;
       }
       sync_off[i] = static_cast<int64_t>(words);
@@ -450,9 +440,7 @@ struct ls_runner {
         const CUtensorMap* mb = map_b(static_cast<int>(p.tc.bn));
         if (!mb) return false;
         TcLaunch L;
-        const TcGeom g = tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n,
-                                 p.tc.grid_n);
-        const CUtensorMap* ma = map_a(128 / g.mc);
+        const CUtensorMap* ma = map_a(128);
         if (!ma) return false;
         L.tmap_a = ma;
         L.tmap_b = mb;
@@ -471,7 +459,6 @@ struct ls_runner {
         L.grid_m = static_cast<int>(p.tc.grid_m);
         L.grid_n = static_cast<int>(p.tc.grid_n);
         L.smem_bytes = static_cast<int>(p.tc.smem_bytes);
-        L.direct = p.tc.direct;
         L.trace = trace;
         L.sync = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
                      ? tcsync + sync_off[static_cast<size_t>(slot)]
