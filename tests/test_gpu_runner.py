@@ -229,7 +229,8 @@ def test_conv2d_general_path_bit_exact(dtype):
     progs = [p["program"] for p in pop]
     plans = r.plan_programs(progs)
     inlined = [i for i, p in enumerate(progs)
-               if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"]
+               if len([b for b in json.loads(p)["buffers"]]) == 3 and plans[i]["status"] == "OK"
+               and plans[i]["family"] != "nestgen"]
     # nest-generic candidates at this shape run the whole conv in <= 56
     # interpreted threads (seconds each); their bit-exactness is covered on the
     # ragged conv in test_gpu_e2e.py::test_ragged_shapes_every_candidate_exact
