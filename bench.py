@@ -149,15 +149,22 @@ def reference_search(e0_json, dtype, device, trials=64):
     t0 = time.perf_counter()
     ref = ls.tune(e0, ls.default_space(), cfg)
     t_ref = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    hw = plugin.tune(e0, ls.default_space(), cfg, mode="hardware", device=device, dtype=dtype,
-                     min_repeats=3, max_repeats=50, target_ms=0.05, timeout_ms=5.0, timeout_factor=10.0)
-    t_hw = time.perf_counter() - t0
-    return {"space": "reference default space", "trials": trials, "seed": 0, "cores": 1,
-            "reference_cpu": {"wall_s": t_ref, "trials_per_s": len(ref.log) / t_ref,
-                              "best": str(ref.best_latency), "unit": "simulated cycles"},
-            "b200_hardware": {"wall_s": t_hw, "trials_per_s": len(hw.log) / t_hw,
-                              "best_ns": float(hw.best_latency), "speedup_vs_e0": hw.speedup}}
+    out = {"space": "reference default space", "trials": trials, "seed": 0, "cores": 1,
+           "reference_cpu": {"wall_s": t_ref, "trials_per_s": len(ref.log) / t_ref,
+                             "best": str(ref.best_latency), "unit": "simulated cycles"}}
+    # the same search with the B200 seams: native trace replay with the
+    # look-ahead (default), native replay alone, and the reference's Python
+    # replay -- K7 featurize launches counted for each
+    for name, nr, la in (("b200_hardware", True, True), ("b200_hardware_no_lookahead", True, False),
+                         ("b200_hardware_python_replay", False, False)):
+        t0 = time.perf_counter()
+        hw = plugin.tune(e0, ls.default_space(), cfg, mode="hardware", device=device, dtype=dtype,
+                         native_replay=nr, lookahead=la, min_repeats=3, max_repeats=50, target_ms=0.05,
+                         timeout_ms=5.0, timeout_factor=10.0)
+        t_hw = time.perf_counter() - t0
+        out[name] = {"wall_s": t_hw, "trials_per_s": len(hw.log) / t_hw, "best_ns": float(hw.best_latency),
+                     "speedup_vs_e0": hw.speedup, **plugin.last_tune_stats}
+    return out
 
 
 def cpu_baseline(programs, model, budget_s=8.0):

@@ -206,6 +206,21 @@ ls_status ls_replay_batch(ls_replayer* r, const char* const* traces, const size_
                           ls_replay_result* out);
 void ls_replay_free(ls_replay_result* res, int n);
 void ls_replayer_destroy(ls_replayer* r);
+/* Look-ahead: every single-decision neighbour of each
+ * member trace -- exactly the traces `mutate` (src/trace.py:287-309) can
+ * propose -- is replayed on the host pool (a member is replayed once, each
+ * neighbour from a snapshot before its changed decision).  The result holds
+ * the programs of the structural hashes this replayer has not handed out
+ * before (to be featurized in one batch); neighbours expanded earlier are
+ * skipped.  Strings live until ls_neighbours_destroy.  stats: replayed,
+ * accepted, rejected, deferred. */
+typedef struct ls_neighbours ls_neighbours;
+ls_status ls_replay_neighbours(ls_replayer* r, const char* const* traces, const size_t* lens, int n,
+                               ls_neighbours** out);
+ls_status ls_neighbours_count(ls_neighbours* nb, int* count);
+ls_status ls_neighbours_get(ls_neighbours* nb, int i, uint64_t* hash, const char** program);
+ls_status ls_neighbours_stats(ls_neighbours* nb, int64_t* out4);
+void ls_neighbours_destroy(ls_neighbours* nb);
 /* ir.structural_hash of a serialized program */
 ls_status ls_program_hash(const char* program, size_t len, uint64_t* out);
 

@@ -21,6 +21,7 @@
 // caller replays that trace with the reference itself and gets the same
 // exception -- behaviour stays identical by construction.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <functional>
 #include <cstdint>
@@ -29,6 +30,8 @@
 #include <deque>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <unordered_set>
 #include <optional>
 #include <set>
 #include <stdexcept>
@@ -976,6 +979,7 @@ const IntrInfo* intrinsic(const std::string& n) {
 enum RefKind : uint8_t { RK_BLOCK, RK_LOOP, RK_RV };
 enum LocKind : uint8_t { L_ROOT, L_INLINE, L_LOOP };
 struct Ref {
+  int idx = -1;  // position in the state's handle table
   std::string id;
   RefKind k;
   std::string payload;  // block name / loop var
@@ -1063,11 +1067,15 @@ class State {
  public:
   Prog prog;
   std::string text;  // recorded (normalized) instructions, serialize_trace lines
-  explicit State(Prog p) : prog(std::move(p)) {}
+  // e0_vars: the loop variables of the workload program, the only names a
+  // fresh "x<n>" variable can collide with
+  State(Prog p, const std::set<std::string>* e0_vars) : prog(std::move(p)), e0_vars_(e0_vars) {}
 
+  Ref* ref_at(int i) { return &refs_[static_cast<size_t>(i)]; }
   Ref* new_ref(RefKind k, std::string payload) {
     refs_.emplace_back();
     Ref& r = refs_.back();
+    r.idx = static_cast<int>(refs_.size()) - 1;
     r.id = "%" + std::to_string(ref_counter_++);
     r.k = k;
     r.payload = std::move(payload);
@@ -1082,6 +1090,17 @@ class State {
       for (size_t i = 0; i < d.size(); ++i) m += (i ? "; " : "") + d[i];
       sched_err(m);
     }
+    prog = std::move(p);
+  }
+  // split / fuse / reorder / set_kind applied to a valid program can only
+  // produce invalid IR through a fresh loop variable that collides with an
+  // existing one (every index they write is affine or a floordiv/mod of a
+  // fresh variable by a positive constant, every variable they introduce is
+  // bound by the loop they create, buffers and blocks are untouched); skip
+  // the whole-program validate_ir then -- its verdict is known to be empty
+  void set_program_checked_vars(Prog p, const std::vector<std::string>& fresh) {
+    for (const auto& v : fresh)
+      if (!e0_vars_ || e0_vars_->count(v)) return set_program(std::move(p));
     prog = std::move(p);
   }
   Prog with_root(std::vector<SP> root) const {
@@ -1214,7 +1233,7 @@ class State {
     std::vector<SP> nest;
     for (const SP& s : node->body) nest.push_back(substitute_stmt(s, m));
     for (size_t i = nv.size(); i-- > 0;) nest = {mk_loop(nv[i], vals[i], "serial", std::move(nest))};
-    set_program(with_root(replace_stmt(prog.root, path, nest)));
+    set_program_checked_vars(with_root(replace_stmt(prog.root, path, nest)), nv);
     kill_loops({node->var});
     std::vector<Ref*> refs;
     for (const auto& v : nv) refs.push_back(new_ref(RK_LOOP, v));
@@ -1295,7 +1314,7 @@ class State {
     std::vector<SP> body;
     for (const SP& s : inner) body.push_back(substitute_stmt(s, m));
     SP fused = mk_loop(fv, prod(ext), "serial", std::move(body));
-    set_program(with_root(replace_stmt(prog.root, chain[0].first, {fused})));
+    set_program_checked_vars(with_root(replace_stmt(prog.root, chain[0].first, {fused})), {fv});
     std::set<std::string> dead;
     for (const auto& pl : chain) dead.insert(pl.second->var);
     kill_loops(dead);
@@ -1315,7 +1334,7 @@ class State {
       const SP& n = resolved[i].second;
       nest = {mk_loop(n->var, n->extent, n->kind, std::move(nest))};
     }
-    set_program(with_root(replace_stmt(prog.root, chain[0].first, nest)));
+    set_program_checked_vars(with_root(replace_stmt(prog.root, chain[0].first, nest)), {});
     record("reorder", {enc(loops)}, Value::obj(), {});
   }
 
@@ -1323,7 +1342,7 @@ class State {
     auto [path, node] = resolve_loop(loop);
     auto n = std::make_shared<St>(*node);
     n->kind = kind;
-    set_program(with_root(replace_stmt(prog.root, path, {n})));
+    set_program_checked_vars(with_root(replace_stmt(prog.root, path, {n})), {});
     record(op, {enc(loop)}, Value::obj(), {});
   }
   void require_data_parallel(const SP& node, const char* what) {
@@ -2003,6 +2022,7 @@ class State {
   }
 
  private:
+  const std::set<std::string>* e0_vars_ = nullptr;
   std::deque<Ref> refs_;
   int64_t ref_counter_ = 0;
   int64_t var_counter_ = 0;
@@ -2029,28 +2049,76 @@ std::map<std::string, double> g_prof;
 #endif
 struct Workload {
   Prog e0;
+  std::string text;  // e0 as serialized
   uint64_t hash = 0;
+  std::set<std::string> loop_vars;  // of e0
+  uint64_t serial = 0;              // identity for the per-thread copies
 };
 
-Arg resolve_arg(const Value& x, std::unordered_map<std::string, Ref*>& env, int index) {
+// Every state shares e0's nodes; replaying on several host threads at once
+// would make all of them bump the same shared_ptr reference counts (one
+// contended cache line per node -- measured: no speed-up at 8 threads), so
+// each thread replays from its own deep copy of e0.
+const Prog& local_e0(const Workload& w) {
+  thread_local std::unordered_map<uint64_t, Prog> copies;
+  auto it = copies.find(w.serial);
+  if (it != copies.end()) return it->second;
+  if (copies.size() > 64) copies.clear();
+  Prog p;
+  program_from(w.text, &p);
+  return copies.emplace(w.serial, std::move(p)).first->second;
+}
+
+// replay's `env` (src/trace.py:179-183): trace id -> handle of this state,
+// by index so a copied state (a neighbour's prefix snapshot) keeps it valid
+struct Env {
+  std::vector<int> num;                      // "%<k>" -> handle index, -1 unbound
+  std::unordered_map<std::string, int> other;
+  static int numeric(const std::string& id) {
+    if (id.size() < 2 || id.size() > 9 || id[0] != '%') return -1;
+    int v = 0;
+    for (size_t i = 1; i < id.size(); ++i) {
+      if (id[i] < '0' || id[i] > '9') return -1;
+      v = v * 10 + (id[i] - '0');
+    }
+    if (id.size() > 2 && id[1] == '0') return -1;  // "%01" is not "%1"
+    return v;
+  }
+  int find(const std::string& id) const {
+    const int k = numeric(id);
+    if (k >= 0) return static_cast<size_t>(k) < num.size() ? num[static_cast<size_t>(k)] : -1;
+    auto it = other.find(id);
+    return it == other.end() ? -1 : it->second;
+  }
+  void set(const std::string& id, int ref) {
+    const int k = numeric(id);
+    if (k >= 0) {
+      if (static_cast<size_t>(k) >= num.size()) num.resize(static_cast<size_t>(k) + 1, -1);
+      num[static_cast<size_t>(k)] = ref;
+    } else {
+      other[id] = ref;
+    }
+  }
+};
+
+Arg resolve_arg(const Value& x, State& st, const Env& env, int index) {
   Arg a;
   if (x.t == Value::Str && !x.s.empty() && x.s[0] == '%') {
-    auto it = env.find(x.s);
-    if (it == env.end()) throw ReplayErr{index, "unresolved reference " + x.s};
-    a.ref = it->second;
+    const int r = env.find(x.s);
+    if (r < 0) throw ReplayErr{index, "unresolved reference " + x.s};
+    a.ref = st.ref_at(r);
     return a;
   }
   if (x.t == Value::Arr) {
     a.is_list = true;
-    for (const Value& i : x.a) a.list.push_back(resolve_arg(i, env, index));
+    for (const Value& i : x.a) a.list.push_back(resolve_arg(i, st, env, index));
     return a;
   }
   a.val = &x;
   return a;
 }
 
-void bind_outputs(const Value& instr, const std::vector<Ref*>& refs, std::unordered_map<std::string, Ref*>& env, int index,
-          const std::string& what) {
+void bind_outputs(const Value& instr, const std::vector<Ref*>& refs, Env& env, int index, const std::string& what) {
   const Value* outs = instr.get("outputs");
   static const Value empty = Value::arr();
   if (!outs) outs = &empty;
@@ -2060,16 +2128,19 @@ void bind_outputs(const Value& instr, const std::vector<Ref*>& refs, std::unorde
                                std::to_string(outs->a.size())};
   for (size_t k = 0; k < refs.size(); ++k) {
     if (outs->a[k].t != Value::Str) defer("output id");
-    env[outs->a[k].s] = refs[k];
+    env.set(outs->a[k].s, refs[k]->idx);
   }
 }
 
-Outcome replay_one(const Workload& w, std::string_view text) {
-  Outcome out;
-  // deserialize_trace (src/trace.py:95-125) of serialize_trace output
+// deserialize_trace (src/trace.py:95-125) of serialize_trace output
+struct Parsed {
   std::vector<Value> instrs;
   bool have_hash = false;
   Value whash;
+  std::string err;  // non-empty: not a trace the native replay takes (DEFER)
+};
+Parsed parse_trace(std::string_view text) {
+  Parsed P;
   size_t pos = 0;
   int lineno = 0;
   while (pos < text.size()) {
@@ -2083,123 +2154,272 @@ Outcome replay_one(const Workload& w, std::string_view text) {
     if (blank) continue;
     Value doc;
     if (!pj::parse(line, &doc) || doc.t != Value::Obj) {
-      out.reason = "unparsable trace line";
-      return out;
+      P.err = "unparsable trace line";
+      return P;
     }
     if (doc.get("workload_hash") && !doc.get("op")) {
       if (lineno != 1) {
-        out.reason = "misplaced header";
-        return out;
+        P.err = "misplaced header";
+        return P;
       }
-      have_hash = true;
-      whash = *doc.get("workload_hash");
+      P.have_hash = true;
+      P.whash = *doc.get("workload_hash");
       continue;
     }
     if (!doc.get("op")) {
-      out.reason = "missing op";
-      return out;
+      P.err = "missing op";
+      return P;
     }
-    instrs.push_back(std::move(doc));
+    P.instrs.push_back(std::move(doc));
+  }
+  return P;
+}
+
+void check_workload_hash(const Workload& w, const Parsed& P) {
+  if (P.have_hash && P.whash.t != Value::Null) {
+    bool same = P.whash.t == Value::Int &&
+                (P.whash.big ? P.whash.s == std::to_string(w.hash)
+                             : (P.whash.i >= 0 && static_cast<uint64_t>(P.whash.i) == w.hash));
+    if (!same) throw ReplayErr{-1, "trace was recorded against a different workload (structural hash mismatch)"};
+  }
+}
+
+// _step (src/trace.py:201-238) for one instruction
+void step(State& st, Env& env, const Value& ins, int index) {
+  const Value* opv = ins.get("op");
+  if (opv->t != Value::Str) defer("op");
+  const std::string& op = opv->s;
+  static const Value empty_arr = Value::arr(), empty_obj = Value::obj();
+  const Value* inputs = ins.get("inputs");
+  if (!inputs) inputs = &empty_arr;
+  if (inputs->t != Value::Arr) defer("inputs");
+  const Value* attrs = ins.get("attrs");
+  if (!attrs) attrs = &empty_obj;
+  if (attrs->t != Value::Obj) defer("attrs");
+  std::vector<Arg> args;
+  args.reserve(inputs->a.size());
+  for (const Value& x : inputs->a) args.push_back(resolve_arg(x, st, env, index));
+  auto arg = [&](size_t i) -> const Arg& {
+    if (i >= args.size()) defer("missing argument");
+    return args[i];
+  };
+  const Value* decision = ins.get("decision");
+#ifdef LSB_REPLAY_PROFILE
+  auto prof_t0 = std::chrono::steady_clock::now();
+  struct ProfEnd {
+    const std::string& op;
+    std::chrono::steady_clock::time_point t0;
+    ~ProfEnd() { g_prof[op] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); }
+  } prof_end{op, prof_t0};
+#endif
+  try {
+    if (op == "get_blocks") {
+      bind_outputs(ins, st.get_blocks(), env, index, op);
+    } else if (op == "get_loops") {
+      bind_outputs(ins, st.get_loops(arg(0)), env, index, op);
+    } else if (op == "split") {
+      bind_outputs(ins, st.split(arg(0), arg(1)), env, index, op);
+    } else if (op == "fuse") {
+      bind_outputs(ins, {st.fuse(arg(0))}, env, index, op);
+    } else if (op == "reorder") {
+      st.reorder(arg(0));
+    } else if (op == "compute_at") {
+      const Value* loc = attrs->get("location");
+      if (loc && loc->t == Value::Str && loc->s == "root") st.compute_at(arg(0), nullptr);
+      else st.compute_at(arg(0), &arg(1));
+    } else if (op == "inline") {
+      st.inline_block(arg(0));
+    } else if (op == "parallelize") {
+      st.parallelize(arg(0));
+    } else if (op == "vectorize") {
+      st.vectorize(arg(0));
+    } else if (op == "unroll") {
+      st.unroll(arg(0));
+    } else if (op == "tensorize") {
+      st.tensorize(arg(0), attrs->get("intrinsic"));
+    } else if (op == "sample_perfect_tile") {
+      if (!decision || decision->t != Value::Obj) defer("decision");
+      bind_outputs(ins, st.sample_perfect_tile(arg(0), attrs->get("n"), decision->get("tile")), env, index, op);
+    } else if (op == "sample_categorical") {
+      if (!decision || decision->t != Value::Obj) defer("decision");
+      bind_outputs(ins, {st.sample_categorical(attrs->get("candidates"), attrs->get("probs"), decision->get("index"))},
+                   env, index, op);
+    } else if (op == "sample_compute_location") {
+      if (!decision || decision->t != Value::Obj) defer("decision");
+      bind_outputs(ins, {st.sample_compute_location(arg(0), decision->get("index"))}, env, index, op);
+    } else {
+      sched_err("unknown instruction op " + pj::py_repr(op));
+    }
+  } catch (const SchedErr& e) {
+    throw ReplayErr{index, e.msg};
+  }
+}
+
+Outcome finish(const State& st, const Parsed& P) {
+  Outcome out;
+  out.status = LS_REPLAY_ACCEPTED;
+  out.program = serialize(st.prog);
+  out.hash = structural_hash(st.prog);
+  std::string& t = out.trace;
+  if (P.have_hash) {
+    Value h = Value::obj();
+    h.put("workload_hash", P.whash);
+    pj::dump(h, &t);
+    t.push_back('\n');
+  }
+  t += st.text;
+  return out;
+}
+
+Outcome rejected(const ReplayErr& e) {
+  Outcome out;
+  out.status = LS_REPLAY_REJECTED;
+  out.index = e.index;
+  out.reason = e.reason;
+  return out;
+}
+
+Outcome replay_one(const Workload& w, std::string_view text) {
+  Parsed P = parse_trace(text);
+  Outcome out;
+  if (!P.err.empty()) {
+    out.reason = P.err;
+    return out;
   }
   try {
-    if (have_hash && whash.t != Value::Null) {
-      bool same = whash.t == Value::Int &&
-                  (whash.big ? whash.s == std::to_string(w.hash)
-                             : (whash.i >= 0 && static_cast<uint64_t>(whash.i) == w.hash));
-      if (!same)
-        throw ReplayErr{-1, "trace was recorded against a different workload (structural hash mismatch)"};
-    }
-    State st(w.e0);
-    std::unordered_map<std::string, Ref*> env;
-    for (int index = 0; index < static_cast<int>(instrs.size()); ++index) {
-      const Value& ins = instrs[static_cast<size_t>(index)];
-      const Value* opv = ins.get("op");
-      if (opv->t != Value::Str) defer("op");
-      const std::string& op = opv->s;
-      static const Value empty_arr = Value::arr(), empty_obj = Value::obj();
-      const Value* inputs = ins.get("inputs");
-      if (!inputs) inputs = &empty_arr;
-      if (inputs->t != Value::Arr) defer("inputs");
-      const Value* attrs = ins.get("attrs");
-      if (!attrs) attrs = &empty_obj;
-      if (attrs->t != Value::Obj) defer("attrs");
-      std::vector<Arg> args;
-      for (const Value& x : inputs->a) args.push_back(resolve_arg(x, env, index));
-      auto arg = [&](size_t i) -> const Arg& {
-        if (i >= args.size()) defer("missing argument");
-        return args[i];
-      };
-      const Value* decision = ins.get("decision");
-#ifdef LSB_REPLAY_PROFILE
-      auto prof_t0 = std::chrono::steady_clock::now();
-      struct ProfEnd {
-        const std::string& op;
-        std::chrono::steady_clock::time_point t0;
-        ~ProfEnd() { g_prof[op] += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); }
-      } prof_end{op, prof_t0};
-#endif
-      try {
-        if (op == "get_blocks") {
-          bind_outputs(ins, st.get_blocks(), env, index, op);
-        } else if (op == "get_loops") {
-          bind_outputs(ins, st.get_loops(arg(0)), env, index, op);
-        } else if (op == "split") {
-          bind_outputs(ins, st.split(arg(0), arg(1)), env, index, op);
-        } else if (op == "fuse") {
-          bind_outputs(ins, {st.fuse(arg(0))}, env, index, op);
-        } else if (op == "reorder") {
-          st.reorder(arg(0));
-        } else if (op == "compute_at") {
-          const Value* loc = attrs->get("location");
-          if (loc && loc->t == Value::Str && loc->s == "root") st.compute_at(arg(0), nullptr);
-          else st.compute_at(arg(0), &arg(1));
-        } else if (op == "inline") {
-          st.inline_block(arg(0));
-        } else if (op == "parallelize") {
-          st.parallelize(arg(0));
-        } else if (op == "vectorize") {
-          st.vectorize(arg(0));
-        } else if (op == "unroll") {
-          st.unroll(arg(0));
-        } else if (op == "tensorize") {
-          st.tensorize(arg(0), attrs->get("intrinsic"));
-        } else if (op == "sample_perfect_tile") {
-          if (!decision || decision->t != Value::Obj) defer("decision");
-          bind_outputs(ins, st.sample_perfect_tile(arg(0), attrs->get("n"), decision->get("tile")), env, index, op);
-        } else if (op == "sample_categorical") {
-          if (!decision || decision->t != Value::Obj) defer("decision");
-          bind_outputs(ins, {st.sample_categorical(attrs->get("candidates"), attrs->get("probs"), decision->get("index"))},
-               env, index, op);
-        } else if (op == "sample_compute_location") {
-          if (!decision || decision->t != Value::Obj) defer("decision");
-          bind_outputs(ins, {st.sample_compute_location(arg(0), decision->get("index"))}, env, index, op);
-        } else {
-          sched_err("unknown instruction op " + pj::py_repr(op));
-        }
-      } catch (const SchedErr& e) {
-        throw ReplayErr{index, e.msg};
-      }
-    }
-    out.status = LS_REPLAY_ACCEPTED;
-    out.program = serialize(st.prog);
-    out.hash = structural_hash(st.prog);
-    std::string& t = out.trace;
-    if (have_hash) {
-      Value h = Value::obj();
-      h.put("workload_hash", whash);
-      pj::dump(h, &t);
-      t.push_back('\n');
-    }
-    t += st.text;
+    check_workload_hash(w, P);
+    State st(local_e0(w), &w.loop_vars);
+    Env env;
+    for (int index = 0; index < static_cast<int>(P.instrs.size()); ++index)
+      step(st, env, P.instrs[static_cast<size_t>(index)], index);
+    return finish(st, P);
   } catch (const ReplayErr& e) {
-    out.status = LS_REPLAY_REJECTED;
-    out.index = e.index;
-    out.reason = e.reason;
+    return rejected(e);
   } catch (const Defer& d) {
     out.status = LS_REPLAY_DEFER;
     out.reason = d.msg;
   }
   return out;
+}
+
+// ---------------------------------------------------------------------------
+// single-decision neighbourhoods (the look-ahead of SURVEY.md §8f-2): every
+// trace `mutate` (src/trace.py:287-309) can propose from a member, as the
+// reference would serialize it, so a prefetched result is found under the
+// exact key _Validator.candidate computes
+// ---------------------------------------------------------------------------
+
+struct Fp {
+  uint64_t a, b;
+  bool operator==(const Fp& o) const { return a == o.a && b == o.b; }
+};
+struct FpHash {
+  size_t operator()(const Fp& f) const { return static_cast<size_t>(f.a ^ (f.b * 0x9E3779B97F4A7C15ULL)); }
+};
+Fp fingerprint(std::string_view s) {
+  uint64_t a = 1469598103934665603ULL, b = 0x84222325cbf29ce4ULL;
+  for (unsigned char c : s) {
+    a = (a ^ c) * 1099511628211ULL;
+    b = (b ^ c) * 0x100000001b3ULL + 0x9E3779B97F4A7C15ULL;
+    b ^= b >> 29;
+  }
+  return {a, b};
+}
+
+// ordered n-tuples of positive integers with product `extent`
+// (ordered_factorizations, src/schedule.py:77-88; order irrelevant here)
+void factorizations(int64_t extent, int64_t n, std::vector<int64_t>& cur, std::vector<std::vector<int64_t>>* out) {
+  if (n == 1) {
+    cur.push_back(extent);
+    out->push_back(cur);
+    cur.pop_back();
+    return;
+  }
+  for (int64_t d = 1; d <= extent; ++d)
+    if (extent % d == 0) {
+      cur.push_back(d);
+      factorizations(extent / d, n - 1, cur, out);
+      cur.pop_back();
+    }
+}
+
+// the alternative decisions of one sampling instruction (_mutation_domain,
+// src/trace.py:268-284) as rewritten instruction lines; false when the line
+// is not a sampling instruction the enumeration understands
+struct Alt {
+  Value ins;         // the instruction with the alternative decision
+  std::string line;  // its serialize_trace line
+};
+bool neighbour_lines(const Value& ins, std::vector<Alt>* out) {
+  const Value* op = ins.get("op");
+  const Value* dec = ins.get("decision");
+  const Value* attrs = ins.get("attrs");
+  if (!op || op->t != Value::Str || !dec || dec->t != Value::Obj || !attrs || attrs->t != Value::Obj) return false;
+  auto with = [&](const char* key, Value v, const char* key2 = nullptr, Value v2 = Value()) {
+    Value x = ins;
+    Value* d = nullptr;
+    for (auto& kv : x.o)
+      if (kv.first == "decision") d = &kv.second;
+    bool set1 = false, set2 = false;
+    for (auto& kv : d->o) {
+      if (kv.first == key) { kv.second = v; set1 = true; }
+      if (key2 && kv.first == key2) { kv.second = v2; set2 = true; }
+    }
+    if (!set1) d->put(key, v);
+    if (key2 && !set2) d->put(key2, v2);
+    std::string line = pj::dumps(x);
+    out->push_back({std::move(x), std::move(line)});
+  };
+  if (op->s == "sample_perfect_tile") {
+    const Value* e = attrs->get("extent");
+    const Value* n = attrs->get("n");
+    const Value* tile = dec->get("tile");
+    if (!e || !n || !tile || e->t != Value::Int || n->t != Value::Int || tile->t != Value::Arr || e->big || n->big ||
+        e->i < 1 || n->i < 1 || n->i > 8)
+      return false;
+    std::vector<int64_t> cur_tile;
+    for (const Value& x : tile->a) {
+      if (x.t != Value::Int || x.big) return false;
+      cur_tile.push_back(x.i);
+    }
+    std::vector<std::vector<int64_t>> dom;
+    std::vector<int64_t> cur;
+    factorizations(e->i, n->i, cur, &dom);
+    for (const auto& f : dom) {
+      if (f == cur_tile) continue;
+      Value l = Value::arr();
+      for (int64_t x : f) l.a.push_back(Value::integer(x));
+      with("tile", std::move(l));
+    }
+    return true;
+  }
+  if (op->s == "sample_categorical") {
+    const Value* probs = attrs->get("probs");
+    const Value* idx = dec->get("index");
+    if (!probs || probs->t != Value::Arr || !idx || idx->t != Value::Int) return false;
+    std::vector<double> w;
+    for (const Value& p : probs->a) {
+      if (p.t == Value::Float) w.push_back(p.d);
+      else if (p.t == Value::Int && !p.big) w.push_back(static_cast<double>(p.i));
+      else return false;
+    }
+    double total = 0;
+    for (double x : w) total += x;
+    for (size_t i = 0; i < w.size(); ++i) {
+      if (!(w[i] > 0) || static_cast<int64_t>(i) == idx->i) continue;
+      with("index", Value::integer(static_cast<int64_t>(i)), "prob", Value::real(w[i] / total));
+    }
+    return true;
+  }
+  if (op->s == "sample_compute_location") {
+    const Value* size = dec->get("size");
+    const Value* idx = dec->get("index");
+    if (!size || !idx || size->t != Value::Int || idx->t != Value::Int || size->big) return false;
+    for (int64_t i = 0; i < size->i; ++i)
+      if (i != idx->i) with("index", Value::integer(i));
+    return true;
+  }
+  return false;
 }
 
 char* dup_cstr(const std::string& s) {
@@ -2215,6 +2435,20 @@ using namespace lsb;
 
 struct ls_replayer {
   rp::Workload w;
+  // keys of every trace replayed through ls_replay_neighbours (128-bit
+  // fingerprints): a later expansion replays only new neighbours
+  std::mutex seen_mu;
+  std::unordered_set<rp::Fp, rp::FpHash> seen;
+  std::unordered_set<uint64_t> hashes;  // structural hashes already handed out
+};
+
+struct ls_neighbours {
+  struct Item {
+    uint64_t hash;
+    std::string program;
+  };
+  std::vector<Item> items;  // programs of structural hashes not seen before
+  int64_t replayed = 0, accepted = 0, rejected = 0, deferred = 0;
 };
 
 extern "C" {
@@ -2234,6 +2468,12 @@ ls_status ls_replayer_create(const char* e0, size_t len, ls_replayer** out) {
     return LS_ERR_PARSE;
   }
   r->w.hash = rp::structural_hash(r->w.e0);
+  r->w.text.assign(e0, len);
+  static std::atomic<uint64_t> serials{1};
+  r->w.serial = serials.fetch_add(1);
+  rp::iter_stmts(r->w.e0.root, [&](const rp::Path&, const rp::St& s) {
+    if (s.k == rp::S_LOOP) r->w.loop_vars.insert(s.var);
+  });
   *out = r.release();
   return LS_OK;
 }
@@ -2263,7 +2503,7 @@ ls_status ls_replay_batch(ls_replayer* r, const char* const* traces, const size_
     x.trace = o.status == LS_REPLAY_ACCEPTED ? rp::dup_cstr(o.trace) : nullptr;
     x.reason = o.status != LS_REPLAY_ACCEPTED ? rp::dup_cstr(o.reason) : nullptr;
   };
-  if (n >= 32) parallel_for(n, one);
+  if (n >= 8) HostPool::get().run(n, one);
   else
     for (int i = 0; i < n; ++i) one(i);
   return LS_OK;
@@ -2290,5 +2530,165 @@ ls_status ls_program_hash(const char* program, size_t len, uint64_t* out) {
 }
 
 void ls_replayer_destroy(ls_replayer* r) { delete r; }
+
+ls_status ls_replay_neighbours(ls_replayer* r, const char* const* traces, const size_t* lens, int n,
+                               ls_neighbours** out) {
+  if (!r || !out || n < 0 || (n > 0 && (!traces || !lens))) {
+    set_error("ls_replay_neighbours: bad arguments");
+    return LS_ERR_ARG;
+  }
+  // per member: the new neighbours (deduplicated against every key this
+  // replayer has expanded), then one replay of the member that snapshots the
+  // state before each mutated instruction, so a neighbour replays only the
+  // suffix from its changed decision
+  struct Res {
+    std::vector<rp::Outcome> outs;
+  };
+  std::vector<Res> per(static_cast<size_t>(n));
+  auto one = [&](int m) {
+    std::string_view text(traces[m], lens[m]);
+    rp::Parsed P = rp::parse_trace(text);
+    if (!P.err.empty()) return;
+    std::vector<std::string_view> lines;
+    size_t pos = 0;
+    while (pos < text.size()) {
+      size_t nl = text.find('\n', pos);
+      if (nl == std::string_view::npos) nl = text.size();
+      lines.push_back(text.substr(pos, nl - pos));
+      pos = nl + 1;
+    }
+    const size_t hdr = P.have_hash ? 1 : 0;
+    if (lines.size() != P.instrs.size() + hdr) return;  // blank lines: leave to the sequential path
+    struct Job {
+      int at;
+      rp::Value ins;
+      std::string key;
+    };
+    std::vector<Job> jobs;
+    for (size_t j = 0; j < P.instrs.size(); ++j) {
+      std::vector<rp::Alt> alts;
+      if (!rp::neighbour_lines(P.instrs[j], &alts)) continue;
+      for (auto& alt : alts) {
+        std::string key;
+        key.reserve(text.size() + 64);
+        for (size_t k = 0; k < lines.size(); ++k) {
+          if (k == j + hdr) key += alt.line;
+          else key.append(lines[k].data(), lines[k].size());
+          key.push_back('\n');
+        }
+        jobs.push_back({static_cast<int>(j), std::move(alt.ins), std::move(key)});
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(r->seen_mu);
+      r->seen.insert(rp::fingerprint(text));
+      std::vector<Job> fresh;
+      for (auto& jb : jobs)
+        if (r->seen.insert(rp::fingerprint(jb.key)).second) fresh.push_back(std::move(jb));
+      jobs.swap(fresh);
+    }
+    if (jobs.empty()) return;
+    auto& items = per[static_cast<size_t>(m)].outs;
+    try {
+      rp::check_workload_hash(r->w, P);
+    } catch (const rp::ReplayErr& e) {
+      for (size_t k = 0; k < jobs.size(); ++k) items.push_back(rp::rejected(e));
+      return;
+    }
+    // the member, with snapshots before every mutated position
+    std::map<int, std::pair<rp::State, rp::Env>> snap;
+    for (const auto& jb : jobs) snap.emplace(jb.at, std::make_pair(rp::State(rp::local_e0(r->w), &r->w.loop_vars), rp::Env()));
+    rp::State st(rp::local_e0(r->w), &r->w.loop_vars);
+    rp::Env env;
+    int failed_at = static_cast<int>(P.instrs.size());
+    rp::Outcome member_fail;
+    try {
+      for (int index = 0; index < static_cast<int>(P.instrs.size()); ++index) {
+        auto it = snap.find(index);
+        if (it != snap.end()) it->second = std::make_pair(st, env);
+        rp::step(st, env, P.instrs[static_cast<size_t>(index)], index);
+      }
+    } catch (const rp::ReplayErr& e) {
+      failed_at = e.index;
+      member_fail = rp::rejected(e);
+    } catch (const rp::Defer& d) {
+      failed_at = -1;  // leave every neighbour to the sequential path
+    }
+    for (auto& jb : jobs) {
+      if (failed_at < 0) break;
+      if (jb.at > failed_at) {  // same prefix up to the member's failure: the same verdict
+        items.push_back(member_fail);
+        continue;
+      }
+      rp::Outcome o;
+      try {
+        auto& sn = snap.at(jb.at);
+        rp::State s2 = sn.first;
+        rp::Env e2 = sn.second;
+        rp::step(s2, e2, jb.ins, jb.at);
+        for (int index = jb.at + 1; index < static_cast<int>(P.instrs.size()); ++index)
+          rp::step(s2, e2, P.instrs[static_cast<size_t>(index)], index);
+        o = rp::finish(s2, P);
+      } catch (const rp::ReplayErr& e) {
+        o = rp::rejected(e);
+      } catch (const rp::Defer& d) {
+        o.status = LS_REPLAY_DEFER;
+        o.reason = d.msg;
+      }
+      items.push_back(std::move(o));
+    }
+  };
+  if (n > 1) HostPool::get().run(n, one);
+  else if (n == 1) one(0);
+  auto nb = std::make_unique<ls_neighbours>();
+  std::lock_guard<std::mutex> lk(r->seen_mu);
+  for (auto& v : per)
+    for (auto& o : v.outs) {
+      ++nb->replayed;
+      if (o.status == LS_REPLAY_ACCEPTED) {
+        ++nb->accepted;
+        if (r->hashes.insert(o.hash).second) nb->items.push_back({o.hash, std::move(o.program)});
+      } else if (o.status == LS_REPLAY_REJECTED) {
+        ++nb->rejected;
+      } else {
+        ++nb->deferred;
+      }
+    }
+  *out = nb.release();
+  return LS_OK;
+}
+
+ls_status ls_neighbours_count(ls_neighbours* nb, int* count) {
+  if (!nb || !count) {
+    set_error("ls_neighbours_count: null argument");
+    return LS_ERR_ARG;
+  }
+  *count = static_cast<int>(nb->items.size());
+  return LS_OK;
+}
+
+ls_status ls_neighbours_get(ls_neighbours* nb, int i, uint64_t* hash, const char** program) {
+  if (!nb || i < 0 || static_cast<size_t>(i) >= nb->items.size() || !hash || !program) {
+    set_error("ls_neighbours_get: bad arguments");
+    return LS_ERR_ARG;
+  }
+  *hash = nb->items[static_cast<size_t>(i)].hash;
+  *program = nb->items[static_cast<size_t>(i)].program.c_str();
+  return LS_OK;
+}
+
+ls_status ls_neighbours_stats(ls_neighbours* nb, int64_t* out4) {
+  if (!nb || !out4) {
+    set_error("ls_neighbours_stats: null argument");
+    return LS_ERR_ARG;
+  }
+  out4[0] = nb->replayed;
+  out4[1] = nb->accepted;
+  out4[2] = nb->rejected;
+  out4[3] = nb->deferred;
+  return LS_OK;
+}
+
+void ls_neighbours_destroy(ls_neighbours* nb) { delete nb; }
 
 }  // extern "C"

@@ -111,6 +111,14 @@ EXPORTS = {
                                        ctypes.POINTER(ReplayResultC)]),
     "ls_replay_free": (None, [ctypes.POINTER(ReplayResultC), ctypes.c_int]),
     "ls_replayer_destroy": (None, [ctypes.c_void_p]),
+    "ls_replay_neighbours": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
+                                            ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_void_p)]),
+    "ls_neighbours_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "ls_neighbours_get": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_char_p)]),
+    "ls_neighbours_stats": (ctypes.c_int, [ctypes.c_void_p, c_i64p]),
+    "ls_neighbours_destroy": (None, [ctypes.c_void_p]),
     "ls_program_hash": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64)]),
     "ls_last_error": (ctypes.c_char_p, []),
     "ls_version": (ctypes.c_char_p, []),

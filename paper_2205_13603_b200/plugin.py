@@ -71,6 +71,7 @@ class ScoreCache:
         self._model = None
         self._scores: dict[bytes, float] = {}
         self.launches = 0
+        self.feat_launches = 0  # K7 featurize launches (the rest score feature rows)
 
     def featurize(self, program, machine_spec=None) -> np.ndarray:
         text = program_text(program)
@@ -78,8 +79,21 @@ class ScoreCache:
         if f is None:
             f = self.scorer.featurize_batch([text], machine_spec)[0]
             self.launches += 1
+            self.feat_launches += 1
             self.features[text] = f
         return f.copy()
+
+    def featurize_many(self, texts, machine_spec=None):
+        """K7 over a batch of program texts in one launch (the look-ahead);
+        memoized like ``featurize``."""
+        todo = [t for t in dict.fromkeys(texts) if t not in self.features]
+        if todo:
+            feats = self.scorer.featurize_batch(todo, machine_spec)
+            self.launches += 1
+            self.feat_launches += 1
+            for t, f in zip(todo, feats):
+                self.features[t] = f
+        return [self.features[t].copy() for t in texts]
 
     def predict(self, features, model) -> float:
         if self.exact:
@@ -121,10 +135,12 @@ def positive_score(s: float) -> float:
 class _Seams:
     """What one ``installed()`` block routes the reference's seams to."""
 
-    def __init__(self, runner, cache, native_replay=True):
+    def __init__(self, runner, cache, native_replay=True, lookahead=False):
         self.runner = runner
         self.cache = cache
         self.native_replay = native_replay
+        self.lookahead = lookahead
+        self.validator = None  # the NativeValidator of this block's search
 
 
 _tls = threading.local()
@@ -165,8 +181,40 @@ def _d_validator(e0, machine_spec=None):
     if cur is not None and cur.native_replay:
         from .replay import native_validator_class
         cls = native_validator_class()
-        return cls(e0, machine_spec) if machine_spec is not None else cls(e0)
+        fb = cur.cache.featurize_many if cur.cache is not None else None
+        v = cls(e0, machine_spec, lookahead=cur.lookahead, featurize_batch=fb)
+        cur.validator = v
+        return v
     return base(e0, machine_spec) if machine_spec is not None else base(e0)
+
+
+def _lookahead_validator():
+    cur = _current()
+    v = cur.validator if cur is not None else None
+    return v if v is not None and v.lookahead else None
+
+
+def _d_evolve(*args, **kw):
+    v = kw.get("validator", args[5] if len(args) > 5 else None)
+    if v is not None and getattr(v, "lookahead", False):
+        v.begin_evolve()
+    return _originals[5](*args, **kw)
+
+
+def _d_mutate(t, rng):
+    v = _lookahead_validator()
+    if v is not None:
+        v.before_mutate(t)   # fills caches only; consumes no randomness
+    return _originals[6](t, rng)
+
+
+def _d_mh_accept(old_pred, new_pred, temperature, rng):
+    ok = _originals[7](old_pred, new_pred, temperature, rng)
+    if ok:
+        v = _lookahead_validator()
+        if v is not None:
+            v.accepted()
+    return ok
 
 
 def _d_predict(self, program, features, model):
@@ -177,7 +225,8 @@ def _d_predict(self, program, features, model):
 
 
 @contextlib.contextmanager
-def installed(runner=None, scorer=None, exact_scores: bool = False, native_replay: bool = True):
+def installed(runner=None, scorer=None, exact_scores: bool = False, native_replay: bool = True,
+              lookahead: bool = True):
     """Route the reference's seams to ``runner`` (Runner protocol) and
     ``scorer`` (Scorer protocol) inside the block.
 
@@ -186,7 +235,10 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
     reference's originals), so concurrent tunes on several threads -- e.g. one
     per GPU -- each see their own runner; the originals are restored when the
     last block exits, also when the search raises.  ``native_replay``
-    routes ``validate_trace`` through the native replay (replay.py)."""
+    routes ``validate_trace`` through the native replay (replay.py);
+    ``lookahead`` (with it) prefetches each generation's single-decision
+    neighbourhood in one native replay batch + one K7 launch, observing
+    ``evolve`` / ``mutate`` / ``mh_accept`` without changing them."""
     global _install_depth, _originals
     ls = loopsched()
     S = ls.search
@@ -194,8 +246,10 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
     with _install_lock:
         if _install_depth == 0:
             vcls = S._Validator
-            _originals = (S._measure_batch, S.simulate_latency, S.featurize, vcls._predict, vcls)
+            _originals = (S._measure_batch, S.simulate_latency, S.featurize, vcls._predict, vcls,
+                          S.evolve, S.mutate, S.mh_accept)
             S._measure_batch, S.simulate_latency, S.featurize = _d_measure, _d_simulate, _d_featurize
+            S.evolve, S.mutate, S.mh_accept = _d_evolve, _d_mutate, _d_mh_accept
             vcls._predict = _d_predict
             _d_validator._ls_dispatch = True
             _d_validator._ls_base = vcls
@@ -204,7 +258,7 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
     st = getattr(_tls, "stack", None)
     if st is None:
         st = _tls.stack = []
-    st.append(_Seams(runner, cache, native_replay))
+    st.append(_Seams(runner, cache, native_replay, lookahead and native_replay))
     try:
         yield cache
     finally:
@@ -215,12 +269,16 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
                 vcls = _originals[4]
                 S._measure_batch, S.simulate_latency, S.featurize, vcls._predict = _originals[:4]
                 S._Validator = vcls
+                S.evolve, S.mutate, S.mh_accept = _originals[5:8]
                 _originals = None
+
+
+last_tune_stats: dict = {}
 
 
 def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
          mode: str = "hardware", runner=None, scorer=None, device: int = 0, dtype: str = "bf16",
-         **runner_opts):
+         native_replay: bool = True, lookahead: bool = True, **runner_opts):
     """The reference's ``tune`` with the B200 seams installed.
 
     mode "hardware": candidates are instantiated and timed on the GPU
@@ -241,8 +299,19 @@ def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
             runner.set_workload(e0)
         else:
             raise ValueError(f"unknown mode {mode!r}")
-    with installed(runner, scorer, exact_scores=(mode == "parity")):
-        return ls.search.tune(e0, generator, config, machine_spec, warm_records)
+    with installed(runner, scorer, exact_scores=(mode == "parity"), native_replay=native_replay,
+                   lookahead=lookahead) as cache:
+        report = ls.search.tune(e0, generator, config, machine_spec, warm_records)
+        v = _current().validator
+        last_tune_stats.clear()
+        last_tune_stats.update({
+            "k7_featurize_launches": cache.feat_launches, "k7_launches": cache.launches,
+            "native_replay": native_replay, "lookahead": lookahead and native_replay,
+            "native_validations": getattr(v, "native_calls", 0),
+            "lookahead_expansions": getattr(v, "expansions", 0),
+            "lookahead_neighbours": getattr(v, "neighbours", 0),
+            "lookahead_prefetched": getattr(v, "prefetched", 0)})
+        return report
 
 
 def tune_with_records(e0, generator, config=None, machine_spec=None, *, runner=None, scorer=None,

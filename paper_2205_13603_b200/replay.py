@@ -65,6 +65,31 @@ class NativeReplayer:
         self._L.ls_replay_free(res, n)
         return out
 
+    def neighbours(self, member_keys):
+        """Replay every single-decision neighbour of each member key not
+        expanded before; returns ([(hash, program_text)] for structural
+        hashes not handed out before, stats dict)."""
+        n = len(member_keys)
+        if n == 0:
+            return [], {"replayed": 0, "accepted": 0, "rejected": 0, "deferred": 0}
+        arr, lens, _keep = native.text_array(member_keys)
+        h = ctypes.c_void_p()
+        native.check(self._L.ls_replay_neighbours(self._h, arr, lens, n, ctypes.byref(h)), "ls_replay_neighbours")
+        try:
+            cnt = ctypes.c_int()
+            native.check(self._L.ls_neighbours_count(h, ctypes.byref(cnt)), "ls_neighbours_count")
+            st = (ctypes.c_int64 * 4)()
+            native.check(self._L.ls_neighbours_stats(h, st), "ls_neighbours_stats")
+            hv, pg = ctypes.c_uint64(), ctypes.c_char_p()
+            get = self._L.ls_neighbours_get
+            out = []
+            for i in range(cnt.value):
+                native.check(get(h, i, ctypes.byref(hv), ctypes.byref(pg)), "ls_neighbours_get")
+                out.append((hv.value, pg.value.decode()))
+            return out, dict(zip(("replayed", "accepted", "rejected", "deferred"), list(st)))
+        finally:
+            self._L.ls_neighbours_destroy(h)
+
     def close(self):
         if self._h:
             self._L.ls_replayer_destroy(self._h)
@@ -161,7 +186,17 @@ def native_validator_class():
         base = S._Validator._ls_base if getattr(S._Validator, "_ls_dispatch", False) else S._Validator
 
         class NativeValidator(base):
-            def __init__(self, e0, machine_spec=None):
+            """``lookahead``: before a generation mutates its members, the
+            single-decision neighbourhood of every member not expanded yet
+            is replayed natively in one batch and the programs of its new
+            structural hashes are featurized in one K7 launch (SURVEY.md
+            §8f-2).  ``evolve``'s sequential proposals then find their
+            features by hash (``features_by_hash``, the reference's own memo)
+            instead of launching K7 one program at a time.  Only that memo
+            is filled: the rng stream, the proposals, the verdicts and every
+            decision of ``evolve`` are the reference's."""
+
+            def __init__(self, e0, machine_spec=None, lookahead=False, featurize_batch=None):
                 if machine_spec is None:
                     super().__init__(e0, ls.MachineSpec())
                 else:
@@ -170,20 +205,81 @@ def native_validator_class():
                 self._lazy = lazy_program_class()
                 self.native_calls = 0
                 self.deferred = 0
+                self.lookahead = lookahead
+                self._featurize_batch = featurize_batch
+                self._pending = []     # member traces not expanded yet
+                self._expanded = set()
+                self._building = False
+                self._last = None
+                self.expansions = 0
+                self.neighbours = 0       # replayed by the look-ahead
+                self.prefetched = 0       # programs featurized ahead
+
+            # -- hooks driven by plugin.installed(lookahead=True) --
+            def begin_evolve(self):
+                self._building = True   # candidates returned until the first mutate are members
+
+            def accepted(self):
+                if self._last is not None:  # mh_accept kept the proposal just returned
+                    self._pending.append(self._last.trace)
+
+            def before_mutate(self, t):
+                self._building = False
+                k = getattr(t, "_ls_key", None) or ls.trace.serialize_trace(t)
+                if k in self._expanded:
+                    return
+                keys = []
+                for m in self._pending + [t]:
+                    mk = getattr(m, "_ls_key", None) or ls.trace.serialize_trace(m)
+                    if mk not in self._expanded:
+                        self._expanded.add(mk)
+                        keys.append(mk)
+                self._pending = []
+                self._expand(keys)
+
+            def _expand(self, keys):
+                new, stats = self._rp.neighbours(keys)
+                self.expansions += 1
+                self.neighbours += stats["replayed"]
+                new = [(h, p) for h, p in new if h not in self.features_by_hash]
+                self.prefetched += len(new)
+                if not new:
+                    return
+                if self._featurize_batch is not None:
+                    feats = self._featurize_batch([p for _, p in new], self.machine_spec)
+                else:
+                    feats = [S.featurize(self._lazy(p), self.machine_spec) for _, p in new]
+                for (h, _), f in zip(new, feats):
+                    self.features_by_hash[h] = f
+
+            def _note(self, cand):
+                self._last = cand
+                if cand is not None and self._building:
+                    self._pending.append(cand.trace)
+                return cand
 
             def candidate(self, t, model):
                 key = ls.trace.serialize_trace(t)
                 if key in self.cache:
-                    return self._revive(self.cache[key], model)
+                    return self._note(self._revive(self.cache[key], model))
                 (st, _idx, h, prog, norm, _reason), = self._rp.validate([key])
                 self.native_calls += 1
                 if st == REJECTED:
                     self.cache[key] = None
-                    return None
+                    return self._note(None)
                 if st == DEFER:
                     self.deferred += 1
-                    return base.candidate(self, t, model)
-                return self._store_native(key, normalized_trace(key, norm, t), self._lazy(prog), h, model)
+                    return self._note(base.candidate(self, t, model))
+                return self._note(self._store_native(key, self._trace(key, norm, t), self._lazy(prog), h, model))
+
+            def from_replay(self, t, program, model):
+                return self._note(base.from_replay(self, t, program, model))
+
+            @staticmethod
+            def _trace(key, norm, t):
+                tr = normalized_trace(key, norm, t)
+                object.__setattr__(tr, "_ls_key", norm)  # serialize_trace(tr), for the look-ahead
+                return tr
 
             def prevalidate(self, traces):
                 """Validate a batch of traces in one native call and store the

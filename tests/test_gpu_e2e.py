@@ -97,3 +97,26 @@ def test_ragged_shapes_every_candidate_exact(build, dtype):
             one, = r.measure_programs([p])
             assert np.array_equal(r.last_output().astype(np.float64), want), x["cfg"]
     r.close()
+
+
+@pytest.mark.parametrize("name", ["gmm512", "bert_ffn"])
+def test_lookahead_cuts_k7_launches_and_keeps_the_report(name):
+    # with the look-ahead every generation's single-decision
+    # neighbourhood is featurized in one K7 batch; the parity-mode report
+    # stays the committed reference report and K7 featurize launches per tune
+    # drop by more than 10x
+    from paper_2205_13603_b200 import plugin, tensor_core as T
+    from paper_2205_13603_b200.refapi import loopsched
+    ls = loopsched()
+    want = json.load(open(os.path.join(GOLDEN, f"tune_{name}.json")))
+    e0, space = {"gmm512": (ls.gmm(512, 512, 512), ls.default_space_config()),
+                 "bert_ffn": (ls.gmm(128, 768, 3072), T.b200_space_config())}[name]
+    launches = {}
+    for la in (False, True):
+        report = plugin.tune(e0, T.space_from_config(space), ls.SearchConfig(trials=64, seed=0), mode="parity",
+                             lookahead=la)
+        got = report.to_json(timestamp=False)
+        assert [g["hash"] for g in got["log"]] == [w["hash"] for w in want["log"]]
+        assert got["best"] == want["best"]
+        launches[la] = plugin.last_tune_stats["k7_featurize_launches"]
+    assert launches[True] * 10 < launches[False], launches

@@ -98,10 +98,33 @@ def test_tune_with_native_validator_is_byte_identical(task):
         e0, gen = ls.gmm(128, 768, 3072), b200_space()
     cfg = S.SearchConfig(trials=48, seed=0)
     ref = S.tune(e0, gen, cfg)
-    with plugin.installed(native_replay=True):
+    with plugin.installed(native_replay=True, lookahead=False):
         assert S._Validator is not None and getattr(S._Validator, "_ls_dispatch", False)
         nat = S.tune(e0, gen, cfg)
     assert not getattr(S._Validator, "_ls_dispatch", False)  # restored
+    a = json.dumps(ref.to_json(timestamp=False), sort_keys=True)
+    b = json.dumps(nat.to_json(timestamp=False), sort_keys=True)
+    assert a == b
+
+
+@needs_reference
+def test_lookahead_prefetch_keeps_the_tune_byte_identical():
+    # the look-ahead replays every single-decision neighbour of each new
+    # member and featurizes their programs ahead (here on the host: no GPU
+    # scorer installed); the search must not change at all
+    from paper_2205_13603_b200 import plugin
+    from paper_2205_13603_b200.refapi import loopsched
+    ls = loopsched()
+    S = ls.search
+    e0 = ls.gmm(64, 64, 64)
+    gen = ls.spaces.space_from_config({"modules": [{"mlt": {"structure": "SSRSR"}}, {"auto_inline": {}},
+                                                   {"pvu": {"widths": [4, 8]}}]})
+    cfg = S.SearchConfig(trials=24, batch=8, population=12, generations=2, seed=3)
+    ref = S.tune(e0, gen, cfg)
+    with plugin.installed(native_replay=True, lookahead=True):
+        nat = S.tune(e0, gen, cfg)
+        v = plugin._current().validator
+        assert v is not None and v.expansions > 0 and v.neighbours > 0 and v.prefetched > 0
     a = json.dumps(ref.to_json(timestamp=False), sort_keys=True)
     b = json.dumps(nat.to_json(timestamp=False), sort_keys=True)
     assert a == b
