@@ -175,6 +175,39 @@ def normalized_trace(key: str, text: str, t):
 
 
 _NATIVE_VALIDATOR = None
+_LAZY_CAND = None
+
+
+def _lazy_candidate_class():
+    """The reference's ``Candidate`` (`src/search.py:63-69`) whose ``features``
+    and ``predicted`` are materialized on first access by the owning
+    validator's batched featurization (the look-ahead)."""
+    global _LAZY_CAND
+    if _LAZY_CAND is None:
+        S = loopsched().search
+
+        class LazyCandidate(S.Candidate):
+            def __init__(self, trace, program, h, owner, model, text):  # noqa: D107
+                self.trace = trace
+                self.program = program
+                self.program_hash = h
+                self._owner, self._model, self._text = owner, model, text
+                self._f = self._p = None
+
+            @property
+            def features(self):
+                if self._f is None:
+                    self._owner._flush_lazy()
+                return self._f
+
+            @property
+            def predicted(self):
+                if self._f is None:
+                    self._owner._flush_lazy()
+                return self._p
+
+        _LAZY_CAND = LazyCandidate
+    return _LAZY_CAND
 
 
 def native_validator_class():
@@ -211,6 +244,7 @@ def native_validator_class():
                 self._expanded = set()
                 self._building = False
                 self._last = None
+                self._lazies = []
                 self.expansions = 0
                 self.neighbours = 0       # replayed by the look-ahead
                 self.prefetched = 0       # programs featurized ahead
@@ -273,7 +307,44 @@ def native_validator_class():
                 return self._note(self._store_native(key, self._trace(key, norm, t), self._lazy(prog), h, model))
 
             def from_replay(self, t, program, model):
-                return self._note(base.from_replay(self, t, program, model))
+                # a fresh (resampled) candidate: with the look-ahead its
+                # features are computed lazily, all pending ones in one K7
+                # batch on first use (evolve reads no feature or prediction
+                # until the population is complete)
+                if not self.lookahead:
+                    return self._note(base.from_replay(self, t, program, model))
+                key = ls.trace.serialize_trace(t)
+                cand = self.cache.get(key)
+                if cand is not None:
+                    return self._note(self._revive(cand, model))
+                text = ls.ir.serialize(program)
+                h = program_hash(text)
+                if h in self.features_by_hash:
+                    return self._note(self._store_native(key, t, program, h, model))
+                lazy = _lazy_candidate_class()(t, program, h, self, model, text)
+                self._lazies.append(lazy)
+                self.cache[key] = lazy
+                return self._note(lazy)
+
+            def _flush_lazy(self):
+                todo = [c for c in self._lazies if c._f is None]
+                self._lazies = []
+                texts = {}
+                for c in todo:
+                    if c.program_hash not in self.features_by_hash:
+                        texts.setdefault(c.program_hash, c._text)
+                if texts:
+                    hs = list(texts)
+                    if self._featurize_batch is not None:
+                        feats = self._featurize_batch([texts[h] for h in hs], self.machine_spec)
+                    else:
+                        feats = [S.featurize(self._lazy(texts[h]), self.machine_spec) for h in hs]
+                    for h, f in zip(hs, feats):
+                        self.features_by_hash[h] = f
+                    self.prefetched += len(hs)
+                for c in todo:
+                    c._f = self.features_by_hash[c.program_hash]
+                    c._p = self._predict(c.program, c._f, c._model)
 
             @staticmethod
             def _trace(key, norm, t):
