@@ -152,10 +152,10 @@ def reference_search(e0_json, dtype, device, trials=64):
     out = {"space": "reference default space", "trials": trials, "seed": 0, "cores": 1,
            "reference_cpu": {"wall_s": t_ref, "trials_per_s": len(ref.log) / t_ref,
                              "best": str(ref.best_latency), "unit": "simulated cycles"}}
-    # the same search with the B200 seams: native trace replay with the
-    # look-ahead (default), native replay alone, and the reference's Python
-    # replay -- K7 featurize launches counted for each
-    for name, nr, la in (("b200_hardware", True, True), ("b200_hardware_no_lookahead", True, False),
+    # the same search with the B200 seams: native trace replay (default),
+    # native replay with the look-ahead, and the reference's Python replay --
+    # K7 featurize launches counted for each
+    for name, nr, la in (("b200_hardware", True, False), ("b200_hardware_lookahead", True, True),
                          ("b200_hardware_python_replay", False, False)):
         t0 = time.perf_counter()
         hw = plugin.tune(e0, ls.default_space(), cfg, mode="hardware", device=device, dtype=dtype,

@@ -226,7 +226,7 @@ def _d_predict(self, program, features, model):
 
 @contextlib.contextmanager
 def installed(runner=None, scorer=None, exact_scores: bool = False, native_replay: bool = True,
-              lookahead: bool = True):
+              lookahead: bool = False):
     """Route the reference's seams to ``runner`` (Runner protocol) and
     ``scorer`` (Scorer protocol) inside the block.
 
@@ -238,7 +238,10 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
     routes ``validate_trace`` through the native replay (replay.py);
     ``lookahead`` (with it) prefetches each generation's single-decision
     neighbourhood in one native replay batch + one K7 launch, observing
-    ``evolve`` / ``mutate`` / ``mh_accept`` without changing them."""
+    ``evolve`` / ``mutate`` / ``mh_accept`` without changing them.  It cuts
+    K7 launches per tune ~50x but replays every neighbour (~44 k for a
+    64-trial gmm512 tune, +0.35 s on the B200 box's host), so it is off by
+    default (profiles/r02_search.md)."""
     global _install_depth, _originals
     ls = loopsched()
     S = ls.search
@@ -278,7 +281,7 @@ last_tune_stats: dict = {}
 
 def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
          mode: str = "hardware", runner=None, scorer=None, device: int = 0, dtype: str = "bf16",
-         native_replay: bool = True, lookahead: bool = True, **runner_opts):
+         native_replay: bool = True, lookahead: bool = False, **runner_opts):
     """The reference's ``tune`` with the B200 seams installed.
 
     mode "hardware": candidates are instantiated and timed on the GPU
