@@ -230,8 +230,8 @@ void launch_naive(const void* x, const void* y, float* c, const Strides& s, bool
 // (timed, deadline-armed) run would charge the module load to the candidate.
 void preload_simt_kernels() {
   simt::SArgs a{};
-  for (int i = 0; i < 8; ++i)
-    for (int j = 0; j < 8; ++j)
+  for (int i = 0; i < kSimtTiles; ++i)
+    for (int j = 0; j < kSimtTiles; ++j)
       for (simt::SimtLauncher f : {simt::launcher_f32_fast(i, j), simt::launcher_f32_chk(i, j),
                                    simt::launcher_bf16_fast(i, j), simt::launcher_bf16_chk(i, j)})
         if (f) f(nullptr, nullptr, nullptr, a, dim3(1), 1, static_cast<size_t>(-1), nullptr);
@@ -261,8 +261,7 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
   a.tb = cfg.tb; a.tm = cfg.tm; a.tn = cfg.tn; a.rb = cfg.rb; a.bk = cfg.bk; a.kt = cfg.kt;
   a.deadline = deadline;
   a.timed_out = timed_out;
-  static const bool no_persist = getenv("LSB_SIMT_NOPERSIST") && atoi(getenv("LSB_SIMT_NOPERSIST")) != 0;
-  a.persist = deadline && !no_persist ? 1 : 0;
+  a.persist = deadline ? 1 : 0;
   a.ntn = a.ntm = a.ntb = 1;
   const int64_t bm = cfg.tm * cfg.rm, bn = cfg.tn * cfg.rn;
   const int vw = bf16 ? 8 : 4;
@@ -293,9 +292,8 @@ bool launch_simt(const void* x, const void* y, float* c, const Strides& s, const
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     db_max = v - 2048;
   }
-  static const bool no_db = getenv("LSB_SIMT_NODB") && atoi(getenv("LSB_SIMT_NODB")) != 0;
   const size_t set_words = (a_words + (size_t)cfg.tb * cfg.bk * a.ldb + 3) & ~(size_t)3;
-  a.db = !bf16 && !no_db && cfg.kt > 1 && 2 * set_words * sizeof(float) <= static_cast<size_t>(db_max) ? 1 : 0;
+  a.db = !bf16 && cfg.kt > 1 && 2 * set_words * sizeof(float) <= static_cast<size_t>(db_max) ? 1 : 0;
   if (a.db) smem = 2 * set_words * sizeof(float);
   dim3 grid((unsigned)cfg.gn, (unsigned)cfg.gm, (unsigned)cfg.gb);
   return fn(x, y, c, a, grid, (int)(cfg.tb * cfg.tm * cfg.tn), smem, st) == cudaSuccess;

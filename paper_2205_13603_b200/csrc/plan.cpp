@@ -8,7 +8,7 @@ namespace lsb {
 
 namespace {
 
-const int64_t kTiles[] = {1, 2, 3, 4, 6, 8, 12, 16};
+const int64_t kTiles[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};  // simt_impl.cuh SimtTable
 
 bool fail(std::string* err, const char* m) {
   if (err) *err = m;
@@ -48,7 +48,7 @@ Plan illegal(Plan p, const char* why) {
 }  // namespace
 
 int simt_tile_index(int64_t v) {
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kSimtTiles; ++i)
     if (kTiles[i] == v) return i;
   return -1;
 }
@@ -284,6 +284,24 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
   c.bk = bk; c.kt = kt;
   int64_t bm = c.tm * c.rm, bn = c.tn * c.rn;
   c.smem_bytes = c.tb * c.bk * (bm + bn + 2) * 4 + 16;  // rows padded by up to one word each
+  if (c.smem_bytes > lim.max_smem) {
+    // a long innermost K part is staged in chunks (k-tiles of a divisor of
+    // it, a multiple of 8 when one fits): every thread still sums k in loop
+    // order, so the result is bit-identical to staging the part whole
+    const int64_t per_k = c.tb * (bm + bn + 2) * 4;
+    int64_t best = 0, best8 = 0;
+    for (int64_t d = c.bk - 1; d >= 1; --d) {
+      if (c.bk % d || per_k * d + 16 > lim.max_smem) continue;
+      if (!best) best = d;
+      if (d % 8 == 0) { best8 = d; break; }
+    }
+    const int64_t d = best8 * 2 >= best ? best8 : best;
+    if (d) {
+      c.kt *= c.bk / d;
+      c.bk = d;
+      c.smem_bytes = per_k * d + 16;
+    }
+  }
   int64_t threads = c.tb * c.tm * c.tn;
   int32_t* o = plan.cfg;
   o[0] = static_cast<int32_t>(c.gb); o[1] = static_cast<int32_t>(c.gm); o[2] = static_cast<int32_t>(c.gn);

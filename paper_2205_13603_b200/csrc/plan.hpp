@@ -136,8 +136,11 @@ struct DeviceLimits {
 
 Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim);
 
-// Register-tile lattice compiled ahead of time for the SIMT family.
+// Register-tile lattice compiled ahead of time for the SIMT family: every
+// RM x RN <= 64 over {1,2,3,4,6,8,12,16,24,32,48,64} (the 2^a 3^b divisors
+// of the BERT / ResNet extents).
+constexpr int kSimtTiles = 12;
 bool simt_tile_supported(int64_t rm, int64_t rn);
-int simt_tile_index(int64_t v);  // index into {1,2,3,4,6,8,12,16} or -1
+int simt_tile_index(int64_t v);  // index into the lattice or -1
 
 }  // namespace lsb

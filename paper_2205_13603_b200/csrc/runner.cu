@@ -1019,8 +1019,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   std::atomic<int> enq_done{0};
   std::atomic<bool> enq_stop{false};
   std::thread helper;
-  static const bool no_precapture = getenv("LSB_NO_PRECAPTURE") && atoi(getenv("LSB_NO_PRECAPTURE")) != 0;
-  if (r->opts.flush_l2 == 0 && !order.empty() && !no_precapture) {
+  if (r->opts.flush_l2 == 0 && !order.empty()) {
     helper = std::thread([&] {
       cudaSetDevice(r->device);
       // start only once the enqueue loop is done: capturing beside it slows
@@ -1076,8 +1075,7 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
   int prev = -1;
   for (int i : order) {
     const Plan& p = plans[static_cast<size_t>(i)];
-    static const bool no_gate = getenv("LSB_NO_GATE") && atoi(getenv("LSB_NO_GATE")) != 0;
-    if (in_chunk == 0 && !no_gate) {
+    if (in_chunk == 0) {
       launch_gate(r->gate, ++seq, kGateMaxNs, r->st);
       ++r->launches;
       r->gate_seq = seq;

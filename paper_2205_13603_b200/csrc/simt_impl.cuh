@@ -418,21 +418,32 @@ cudaError_t simt_launch(const void* x, const void* y, float* c, const SArgs& a, 
 
 typedef cudaError_t (*SimtLauncher)(const void*, const void*, float*, const SArgs&, dim3, int, size_t, cudaStream_t);
 
+// only RM x RN <= 64 is instantiated (plan.hpp kSimtTiles)
+template <typename T, int RM, int RN, bool CHK>
+SimtLauncher pick() {
+  if constexpr (RM * RN <= 64) return simt_launch<T, RM, RN, CHK>;
+  else return nullptr;
+}
+
 template <typename T, int RM, bool CHK>
 void fill_row(SimtLauncher* row) {
-  row[0] = 1 * RM <= 64 ? simt_launch<T, RM, 1, CHK> : nullptr;
-  row[1] = 2 * RM <= 64 ? simt_launch<T, RM, 2, CHK> : nullptr;
-  row[2] = 3 * RM <= 64 ? simt_launch<T, RM, 3, CHK> : nullptr;
-  row[3] = 4 * RM <= 64 ? simt_launch<T, RM, 4, CHK> : nullptr;
-  row[4] = 6 * RM <= 64 ? simt_launch<T, RM, 6, CHK> : nullptr;
-  row[5] = 8 * RM <= 64 ? simt_launch<T, RM, 8, CHK> : nullptr;
-  row[6] = 12 * RM <= 64 ? simt_launch<T, RM, 12, CHK> : nullptr;
-  row[7] = 16 * RM <= 64 ? simt_launch<T, RM, 16, CHK> : nullptr;
+  row[0] = pick<T, RM, 1, CHK>();
+  row[1] = pick<T, RM, 2, CHK>();
+  row[2] = pick<T, RM, 3, CHK>();
+  row[3] = pick<T, RM, 4, CHK>();
+  row[4] = pick<T, RM, 6, CHK>();
+  row[5] = pick<T, RM, 8, CHK>();
+  row[6] = pick<T, RM, 12, CHK>();
+  row[7] = pick<T, RM, 16, CHK>();
+  row[8] = pick<T, RM, 24, CHK>();
+  row[9] = pick<T, RM, 32, CHK>();
+  row[10] = pick<T, RM, 48, CHK>();
+  row[11] = pick<T, RM, 64, CHK>();
 }
 
 template <typename T, bool CHK>
 struct SimtTable {
-  SimtLauncher t[8][8];
+  SimtLauncher t[12][12];
   SimtTable() {
     fill_row<T, 1, CHK>(t[0]);
     fill_row<T, 2, CHK>(t[1]);
@@ -442,9 +453,12 @@ struct SimtTable {
     fill_row<T, 8, CHK>(t[5]);
     fill_row<T, 12, CHK>(t[6]);
     fill_row<T, 16, CHK>(t[7]);
+    fill_row<T, 24, CHK>(t[8]);
+    fill_row<T, 32, CHK>(t[9]);
+    fill_row<T, 48, CHK>(t[10]);
+    fill_row<T, 64, CHK>(t[11]);
   }
 };
-
 
 SimtLauncher launcher_f32_fast(int i, int j);
 SimtLauncher launcher_f32_chk(int i, int j);

@@ -41,8 +41,7 @@ bool launch_simta(const void* x, const void* y, float* c, const AffineCfg& A, bo
   a.gm = A.gm; a.gn = A.gn; a.tm = A.tm; a.tn = A.tn; a.bk = A.bk; a.kt = A.kt;
   a.deadline = deadline;
   a.timed_out = timed_out;
-  static const bool no_persist = getenv("LSB_SIMT_NOPERSIST") && atoi(getenv("LSB_SIMT_NOPERSIST")) != 0;
-  a.persist = deadline && !no_persist ? 1 : 0;
+  a.persist = deadline ? 1 : 0;
   a.ntn = a.ntm = 1;
   const size_t smem = static_cast<size_t>(A.smem_bytes);
   cudaError_t e = bf16 ? launch_simta_bf16(x, y, c, a, static_cast<int>(A.rm), static_cast<int>(A.rn), smem, st)

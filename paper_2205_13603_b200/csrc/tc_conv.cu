@@ -374,11 +374,9 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   a.sync = sync;
   // TMA epilogue: the 64 box rows are the 8 x 8 pixels of an NHWC output
   // ([n][p][q][k], row r -> (p0 + r/8, q0 + r%8)) and BN is whole 32-ch chunks
-  static const bool no_tma_epi = getenv("LSB_TC_NOTMAEPI") && atoi(getenv("LSB_TC_NOTMAEPI")) != 0;
   a.tma_epi = 0;
-  static const int full_wait = getenv("LSB_TC_STOREWAIT") ? atoi(getenv("LSB_TC_STOREWAIT")) : 1;
-  a.full_wait = full_wait;
-  if (tmap_c && oshape && !no_tma_epi && a.mode != 1 && g.bn % 32 == 0 && g.cc_w1 == oshape[3] &&
+  a.full_wait = 1;
+  if (tmap_c && oshape && a.mode != 1 && g.bn % 32 == 0 && g.cc_w1 == oshape[3] &&
       g.cc_h1 == oshape[2] * oshape[3]) {
     a.tma_epi = 1;
     for (int d = 0; d < 4; ++d) a.oshape[d] = oshape[d];
