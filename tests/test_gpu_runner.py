@@ -353,3 +353,31 @@ def test_set_workload_consumes_host_inputs_before_returning(name, dtype):
     assert any(x["status"] == "OK" for x in res), res
     assert all(x["mismatches"] == 0 for x in res if x["status"] == "OK"), res
     r.close()
+
+
+def test_simt_wide_register_tiles_and_chunked_k_tiles_exact():
+    # round-2 instantiator coverage: register tiles 24/32/48/64 (the rest of
+    # the 2^a 3^b lattice with RM x RN <= 64) and innermost K parts staged in
+    # chunks when the whole part does not fit in shared memory -- both were
+    # ILLEGAL by convention before; such candidates must be bit-exact
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop[:1024]]
+    r = make_runner("bf16", timeout_ms=200.0)
+    r.set_workload(e0, seed=0)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 0)).values()))
+    plans = r.plan_programs(progs)
+    simt = [i for i, p in enumerate(plans) if p["family"] == "simt" and p["status"] == "OK"]
+    wide = [i for i in simt if max(plans[i]["cfg"][7], plans[i]["cfg"][8]) >= 24][:6]
+    big = sorted(simt, key=lambda i: -plans[i]["cfg"][11])[:6]  # largest smem k-tiles (chunked ones among them)
+    assert len(wide) == 6 and big
+    ok = 0
+    for i in dict.fromkeys(wide + big):
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] in ("OK", "TIMEOUT"), res
+        if res["status"] == "OK":
+            ok += 1
+            assert res["mismatches"] == 0
+            assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
+    assert ok >= 6
+    r.close()

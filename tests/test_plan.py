@@ -49,9 +49,14 @@ def test_simt_mapping_matches_mlt_bands():
         gb, gm, gn, tb, tm, tn, rb, rm, rn, bk, kt = r["cfg"][:11]
         assert gm * tm * rm == 512 and gn * tn * rn == 512 and bk * kt == 512
         assert (gb, tb, rb) == (1, 1, 1)
-        legal = tm * tn <= 1024 and rm * rn <= 64 and rm in (1, 2, 3, 4, 6, 8, 12, 16) \
-            and rn in (1, 2, 3, 4, 6, 8, 12, 16) and bk * (tm * rm + tn * rn + 2) * 4 + 16 <= 231 * 1024
+        # hardware limits only: threads, register tile (the 2^a 3^b lattice
+        # covers every divisor of 512), shared memory after k-chunking
+        lattice = (1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64)
+        legal = tm * tn <= 1024 and rm * rn <= 64 and rm in lattice and rn in lattice \
+            and bk * (tm * rm + tn * rn + 2) * 4 + 16 <= 227 * 1024
         assert (r["status"] == "OK") == legal, r
+        if r["status"] == "OK" and bk > 1:
+            assert 512 % bk == 0
 
 
 def test_bmm_batch_axis_mapping():
