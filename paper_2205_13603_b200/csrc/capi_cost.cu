@@ -224,6 +224,11 @@ struct Workspace {
   double *feats = nullptr, *pred = nullptr;
   int32_t* status = nullptr;
   size_t cap_words = 0, cap_n = 0;
+  // pinned host staging: blob words + offsets in, results out (pageable
+  // copies go through the driver's own staging buffer, several x slower)
+  int64_t* h_in = nullptr;   // [cap_n + 1 offsets][cap_words blob words]
+  uint8_t* h_out = nullptr;  // num | den | feats | pred | status, cap_n each
+  size_t h_in_cap = 0, h_out_cap = 0;
 };
 Workspace g_ws[64];
 
@@ -247,6 +252,20 @@ ls_status grow(Workspace& w, size_t words, size_t n) {
     LSB_CUDA(cudaMalloc(&w.pred, c * 8));
     LSB_CUDA(cudaMalloc(&w.status, c * 4));
     w.cap_n = c;
+  }
+  const size_t in_words = w.cap_n + 1 + w.cap_words;
+  if (in_words > w.h_in_cap) {
+    cudaFreeHost(w.h_in);
+    w.h_in = nullptr;
+    LSB_CUDA(cudaMallocHost(&w.h_in, in_words * 8));
+    w.h_in_cap = in_words;
+  }
+  const size_t out_bytes = w.cap_n * (8 + 8 + 72 + 8 + 4);
+  if (out_bytes > w.h_out_cap) {
+    cudaFreeHost(w.h_out);
+    w.h_out = nullptr;
+    LSB_CUDA(cudaMallocHost(&w.h_out, out_bytes));
+    w.h_out_cap = out_bytes;
   }
   return LS_OK;
 }
@@ -280,27 +299,44 @@ ls_status ls_analyze_batch(int device, const char* const* programs, const size_t
       b[H_STATUS] = LS_PROG_ANALYSIS;
     }
   });
-  std::vector<int64_t> offsets(static_cast<size_t>(n) + 1, 0);
+  const size_t nn = static_cast<size_t>(n);
+  std::vector<int64_t> offsets(nn + 1, 0);
   for (int i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + static_cast<int64_t>(blobs[i].size());
-  std::vector<int64_t> flat(static_cast<size_t>(offsets[n]));
-  for (int i = 0; i < n; ++i) std::copy(blobs[i].begin(), blobs[i].end(), flat.begin() + offsets[i]);
+  const size_t words = static_cast<size_t>(offsets[nn]);
 
   Workspace& w = g_ws[device];
   std::lock_guard<std::mutex> lock(w.mu);
-  if ((st = grow(w, flat.size(), static_cast<size_t>(n))) != LS_OK) return st;
-  const size_t nn = static_cast<size_t>(n);
-  LSB_CUDA(cudaMemcpyAsync(w.blobs, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, w.stream));
-  LSB_CUDA(cudaMemcpyAsync(w.off, offsets.data(), (nn + 1) * 8, cudaMemcpyHostToDevice, w.stream));
+  if ((st = grow(w, words, nn)) != LS_OK) return st;
+  // offsets then the blobs, contiguous in pinned memory: one DMA
+  int64_t* hin = w.h_in;
+  std::copy(offsets.begin(), offsets.end(), hin);
+  int64_t* hblob = hin + nn + 1;
+  parallel_for(n, [&](int i) {
+    std::copy(blobs[static_cast<size_t>(i)].begin(), blobs[static_cast<size_t>(i)].end(), hblob + offsets[i]);
+  });
+  LSB_CUDA(cudaMemcpyAsync(w.off, hin, (nn + 1) * 8, cudaMemcpyHostToDevice, w.stream));
+  LSB_CUDA(cudaMemcpyAsync(w.blobs, hblob, words * 8, cudaMemcpyHostToDevice, w.stream));
   int flags = (num || den ? 1 : 0) | (feats ? 2 : 0) | (pred && model ? 4 : 0);
   launch_analyze(w.blobs, w.off, n, to_dspec(spec), to_dmodel(model), flags, w.num, w.den, w.feats, w.pred,
                  w.status, w.stream);
   LSB_CUDA(cudaGetLastError());
-  if (num) LSB_CUDA(cudaMemcpyAsync(num, w.num, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (den) LSB_CUDA(cudaMemcpyAsync(den, w.den, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (feats) LSB_CUDA(cudaMemcpyAsync(feats, w.feats, nn * 72, cudaMemcpyDeviceToHost, w.stream));
-  if (pred && model) LSB_CUDA(cudaMemcpyAsync(pred, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (status) LSB_CUDA(cudaMemcpyAsync(status, w.status, nn * 4, cudaMemcpyDeviceToHost, w.stream));
+  uint8_t* ho = w.h_out;
+  int64_t* o_num = reinterpret_cast<int64_t*>(ho);
+  int64_t* o_den = o_num + w.cap_n;
+  double* o_feats = reinterpret_cast<double*>(o_den + w.cap_n);
+  double* o_pred = o_feats + 9 * w.cap_n;
+  int32_t* o_status = reinterpret_cast<int32_t*>(o_pred + w.cap_n);
+  if (num) LSB_CUDA(cudaMemcpyAsync(o_num, w.num, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (den) LSB_CUDA(cudaMemcpyAsync(o_den, w.den, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (feats) LSB_CUDA(cudaMemcpyAsync(o_feats, w.feats, nn * 72, cudaMemcpyDeviceToHost, w.stream));
+  if (pred && model) LSB_CUDA(cudaMemcpyAsync(o_pred, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  if (status) LSB_CUDA(cudaMemcpyAsync(o_status, w.status, nn * 4, cudaMemcpyDeviceToHost, w.stream));
   LSB_CUDA(cudaStreamSynchronize(w.stream));
+  if (num) std::memcpy(num, o_num, nn * 8);
+  if (den) std::memcpy(den, o_den, nn * 8);
+  if (feats) std::memcpy(feats, o_feats, nn * 72);
+  if (pred && model) std::memcpy(pred, o_pred, nn * 8);
+  if (status) std::memcpy(status, o_status, nn * 4);
   return LS_OK;
 }
 

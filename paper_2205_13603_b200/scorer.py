@@ -34,6 +34,27 @@ class GpuScorer:
         native.lib()
         self.device = device
 
+    def analyze_arrays(self, texts: Sequence[str], machine_spec=None, model=None):
+        """The batch in the reference Runner's own form, as arrays: exact
+        latency numerators / denominators, features [n,9], predictions [n]
+        (zeros without a model), per-program status -- the same outputs as the
+        CPU reference arm's ``oracle.batch`` (one fused K7+K8 launch)."""
+        n = len(texts)
+        arr, lens, _keep = native.text_array(texts)
+        spec = native.machine_spec_c(machine_spec)
+        num = np.zeros(max(n, 1), np.int64)
+        den = np.zeros(max(n, 1), np.int64)
+        feats = np.zeros((max(n, 1), 9), np.float64)
+        pred = np.zeros(max(n, 1), np.float64)
+        status = np.zeros(max(n, 1), np.int32)
+        mptr = ctypes.byref(native.linear_model_c(model)) if model is not None else None
+        P = native.as_np_ptr
+        native.check(native.lib().ls_analyze_batch(
+            self.device, arr, lens, n, ctypes.byref(spec), mptr, P(num, ctypes.c_int64), P(den, ctypes.c_int64),
+            P(feats, ctypes.c_double), P(pred, ctypes.c_double) if model is not None else None,
+            P(status, ctypes.c_int32)), "ls_analyze_batch")
+        return num[:n], den[:n], feats[:n], pred[:n], status[:n]
+
     def analyze(self, programs: Sequence, machine_spec=None, model=None,
                 want_latency=True, want_features=True):
         """(latencies as Fractions or None, features [n,9] or None,
