@@ -7,7 +7,9 @@
 // pad stage costs nothing -- and the matching [BN x 64] slice of the K-major
 // weight copy.  The lower 64 rows are dead (never written, never read back):
 // the UMMA tile is 128 x BN with half its rows live (M = 64 output pixels
-// per box).
+// per box) -- unless the CTA takes a PAIR of boxes (`pair`, split-K modes 0
+// and 2): box 2j in rows 0..63 and box 2j+1 in rows 64..127 of every stage,
+// one weight slice for both, so every UMMA row is live and the grid halves.
 //
 // Warp roles and pipeline as in tc_gemm.cu (TMA producer lane, single MMA
 // issuer, S-stage mbarrier ring, PDL).  Filter-row parts hoisted above every
@@ -20,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -54,7 +58,8 @@ struct TcConvArgs {
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA, as tc_gemm)
   uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets + [kTcSyncSlots] zeroing flags per tile
   int tma_epi;                // modes 0/2: 128B-swizzled [64 px][32 ch] chunks -> 4-D TMA store / add-reduce
-  int full_wait;              // wait for TMA store / reduce completion before exit (LSB_TC_STOREWAIT=0: smem reads only)
+  int pair;                   // two boxes per CTA (grid y = pairs of boxes)
+  int grid_m;                 // boxes (pair: the odd last pair has one)
   int64_t oshape[4];          // output [n][p][q][k] (decodes the box origin for the C tensor map)
 };
 
@@ -110,7 +115,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const int rows_per = (kRows + S_cl - 1) / S_cl;
   const uint32_t red = a.mode == 1 ? ((stage_end + 15u) & ~15u) : base;
   const uint32_t red_bytes = a.mode == 1 ? static_cast<uint32_t>(S_cl * rows_per * red_ld * 4)
-                                         : static_cast<uint32_t>(kRows * red_ld * 4);
+                                         : static_cast<uint32_t>((a.pair ? 2 : 1) * kRows * red_ld * 4);
   const uint32_t red_end = red + red_bytes;
   const uint32_t bars = ((stage_end > red_end ? stage_end : red_end) + 15u) & ~15u;
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
@@ -147,17 +152,31 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
   if (tr && threadIdx.x == 0) tr[1] = gtime();
 
-  // tile origin: output-pixel box (grid y), channel tile (grid x), split (grid z)
+  // tile origin: output-pixel box (grid y; a pair of boxes with `pair`),
+  // channel tile (grid x), split (grid z)
+  const uint32_t box0 = a.pair ? 2u * blockIdx.y : blockIdx.y;
+  const int nbox = a.pair && static_cast<int>(box0) + 1 < a.grid_m ? 2 : 1;
   Coord o{a.x_n0, a.x_h0, a.x_w0, a.x_c0, 0, 0, a.c0};
-  add_parts(a.m_grid, blockIdx.y, o);
+  add_parts(a.m_grid, box0, o);
   add_parts(a.n_grid, blockIdx.x, o);
+  Coord o1 = o;
+  if (nbox == 2) {
+    o1 = Coord{a.x_n0, a.x_h0, a.x_w0, a.x_c0, 0, 0, a.c0};
+    add_parts(a.m_grid, box0 + 1, o1);
+    add_parts(a.n_grid, blockIdx.x, o1);
+  }
   const KCoord* kc = a.kc + blockIdx.z * a.kt;
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-  float* cbase = a.c + o.cc;
-  auto out_row = [&](int r) { return cbase + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1; };
+  const int live = nbox * kRows;  // accumulator rows that hold output pixels
+  // row r (0..live-1): box r / 64, pixel r % 64 of that box
+  auto out_row = [&](int r) {
+    float* cb = a.c + (r >= kRows ? o1.cc : o.cc);
+    r &= kRows - 1;
+    return cb + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1;
+  };
   const int c4 = a.bn / 4;
   if (a.mode == 2 && warp >= 2) {
     // split-K through L2 (as tc_gemm.cu mode 2): arrival ticket per tile; the
@@ -169,7 +188,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     const uint32_t t = s_ticket;
     if (t % static_cast<uint32_t>(a.splits) == 0) {
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int e = t2; e < kRows * c4; e += 64) {
+      for (int e = t2; e < live * c4; e += 64) {
         const int r = e / c4, cc = (e % c4) * 4;
         *reinterpret_cast<float4*>(out_row(r) + cc) = z;
       }
@@ -180,7 +199,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    const uint32_t stage_bytes = kLiveA + b_bytes;
+    const uint32_t stage_bytes = nbox * kLiveA + b_bytes;
     for (int kt = 0; kt < a.kt; ++kt) {
       const int s = kt % a.stages;
       const uint32_t ph = (kt / a.stages) & 1;
@@ -189,6 +208,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       mbar_expect_tx(full + 8 * s, stage_bytes);
       tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c, static_cast<int>(o.w) + k.w,
                   static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n);
+      if (nbox == 2)  // rows 64..127: the second box (8 KB = 8 swizzle atoms in)
+        tma_load_4d(a0 + s * kStageA + kLiveA, &tmx, full + 8 * s, static_cast<int>(o1.c) + k.c,
+                    static_cast<int>(o1.w) + k.w, static_cast<int>(o1.h) + k.h, static_cast<int>(o1.n) + k.n);
       tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf, static_cast<int>(o.co), 0);
     }
   } else if (warp == 1 && lane == 0) {
@@ -208,7 +230,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     umma_commit(done);
   }
 
-  // ---- epilogue: rows 0..63 (TMEM lanes of warps 0 and 1) ----
+  // ---- epilogue: rows 0..live-1 (TMEM lanes of warps 0-1, and 2-3 for a pair) ----
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
@@ -245,16 +267,17 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       *reinterpret_cast<float4*>(out_row(r_lo + lr2) + cc) = acc;
     }
   } else if (a.tma_epi) {
-    // TMEM rows 0..63 -> [64 px][32 ch] fp32 chunks, 128-byte swizzle (unit q of
-    // row r at q ^ (r & 7)), then one 4-D TMA store / add-reduce per chunk
-    if (warp < 2) {
+    // TMEM rows -> per box [64 px][32 ch] fp32 chunks, 128-byte swizzle (unit
+    // q of row r at q ^ (r & 7)), then one 4-D TMA store / add-reduce per chunk
+    const int nch = a.bn / 32;
+    if (row < live) {
       const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
       for (int c0 = 0; c0 < a.bn; c0 += 32) {
         uint32_t v[32];
         tmem_ld16_nowait(trow + c0, v);
         tmem_ld16_nowait(trow + c0 + 16, v + 16);
         tmem_wait();
-        uint8_t* chunk = gbase + (c0 / 32) * 8192 + row * 128;
+        uint8_t* chunk = gbase + ((row >> 6) * nch + c0 / 32) * 8192 + (row & 63) * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(chunk + ((q ^ (row & 7)) << 4)) =
@@ -273,25 +296,26 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
     if (tr && threadIdx.x == 0) tr[5] = gtime();
     if (threadIdx.x == 0) {
-      int64_t off = o.cc;
-      const int co0 = static_cast<int>(off % a.oshape[3]);
-      off /= a.oshape[3];
-      const int q0 = static_cast<int>(off % a.oshape[2]);
-      off /= a.oshape[2];
-      const int p0 = static_cast<int>(off % a.oshape[1]);
-      const int n0 = static_cast<int>(off / a.oshape[1]);
       fence_proxy_async_global();
-      for (int c0 = 0; c0 < a.bn; c0 += 32) {
-        const uint32_t src = base + (c0 / 32) * 8192;
-        if (a.mode == 2) tma_reduce_add_4d(&tmc, src, co0 + c0, q0, p0, n0);
-        else tma_store_4d(&tmc, src, co0 + c0, q0, p0, n0);
+      for (int b = 0; b < nbox; ++b) {
+        int64_t off = b ? o1.cc : o.cc;
+        const int co0 = static_cast<int>(off % a.oshape[3]);
+        off /= a.oshape[3];
+        const int q0 = static_cast<int>(off % a.oshape[2]);
+        off /= a.oshape[2];
+        const int p0 = static_cast<int>(off % a.oshape[1]);
+        const int n0 = static_cast<int>(off / a.oshape[1]);
+        for (int c0 = 0; c0 < a.bn; c0 += 32) {
+          const uint32_t src = base + (b * nch + c0 / 32) * 8192;
+          if (a.mode == 2) tma_reduce_add_4d(&tmc, src, co0 + c0, q0, p0, n0);
+          else tma_store_4d(&tmc, src, co0 + c0, q0, p0, n0);
+        }
       }
       bulk_commit();
-      if (a.full_wait) bulk_wait_all();
-      else bulk_wait_read();
+      bulk_wait_all();
     }
   } else {
-    if (warp < 2) {
+    if (row < live) {
       float* stg = reinterpret_cast<float*>(gbase) + row * red_ld;
       for (int c0 = 0; c0 < a.bn; c0 += 16) {
         float v[16];
@@ -312,7 +336,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
     if (tr && threadIdx.x == 0) tr[5] = gtime();
     const float* sb = reinterpret_cast<const float*>(gbase);
-    for (int e = threadIdx.x; e < kRows * c4; e += 128) {
+    for (int e = threadIdx.x; e < live * c4; e += 128) {
       const int r = e / c4, cc = (e % c4) * 4;
       const float4 v = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
       if (a.mode == 2) red_add_f4(out_row(r) + cc, v);
@@ -375,7 +399,6 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   // TMA epilogue: the 64 box rows are the 8 x 8 pixels of an NHWC output
   // ([n][p][q][k], row r -> (p0 + r/8, q0 + r%8)) and BN is whole 32-ch chunks
   a.tma_epi = 0;
-  a.full_wait = 1;
   if (tmap_c && oshape && a.mode != 1 && g.bn % 32 == 0 && g.cc_w1 == oshape[3] &&
       g.cc_h1 == oshape[2] * oshape[3]) {
     a.tma_epi = 1;
@@ -386,6 +409,16 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(g.bn)) cols <<= 1;
   a.tmem_cols = cols;
+  // box pairs: every UMMA row live, half the CTAs; needs the doubled staged
+  // tile to fit beside the ring the planner sized
+  a.grid_m = static_cast<int>(g.grid_m);
+  {
+    const int64_t ring = g.stages * (kStageA + g.bn * 64 * 2);
+    const int64_t tile2 = 2LL * kRows * (g.bn + 4) * 4;
+    const int64_t need = 1024 + std::max(ring, tile2) + 16 * g.stages + 64;
+    a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes ? 1 : 0;
+  }
+  const int64_t grid_y = a.pair ? (g.grid_m + 1) / 2 : g.grid_m;
   static bool nonportable = false;
   if (a.mode == 1 && g.splits > 8 && !nonportable) {
     if (cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -395,19 +428,19 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     nonportable = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(g.grid_n), static_cast<unsigned>(g.grid_m), static_cast<unsigned>(g.splits));
+  cfg.gridDim = dim3(static_cast<unsigned>(g.grid_n), static_cast<unsigned>(grid_y), static_cast<unsigned>(g.splits));
   cfg.blockDim = dim3(128, 1, 1);
   cfg.dynamicSmemBytes = static_cast<size_t>(g.smem_bytes);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = a.mode == 1 ? static_cast<unsigned>(g.splits) : 1u;  // mode 2: no cluster
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // mode 1 only: a 1x1x1 cluster launch costs time
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = static_cast<unsigned>(g.splits);
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = a.mode == 1 ? 2 : 1;
   const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
   const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
   const CUtensorMap tcm = a.tma_epi ? *static_cast<const CUtensorMap*>(tmap_c) : tw;
