@@ -8,7 +8,7 @@
 // weight copy.  The lower 64 rows are dead (never written, never read back):
 // the UMMA tile is 128 x BN with half its rows live (M = 64 output pixels
 // per box) -- unless the CTA takes a PAIR of boxes (`pair`, split-K modes 0
-// and 2, grids of more than two CTAs per SM): box 2j in rows 0..63 and box
+// and 2; BN 16 tiles or grids above two CTAs per SM): box 2j in rows 0..63 and box
 // 2j+1 in rows 64..127 of every stage, one weight slice for both, so every
 // UMMA row is live and the grid halves.
 //
@@ -417,11 +417,12 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     const int64_t ring = g.stages * (kStageA + g.bn * 64 * 2);
     const int64_t tile2 = 2LL * kRows * (g.bn + 4) * 4;
     const int64_t need = 1024 + std::max(ring, tile2) + 16 * g.stages + 64;
-    // measured (profiles/r02_conv_pairs.txt): pairing pays only when the
-    // unpaired grid would put more than two CTAs on an SM (BN 16, 3 splits:
-    // 15.6 vs 20.6 us); at <= 2 per SM the extra CTAs hide more latency
+    // measured (profiles/r02_conv_pairs.txt): pairing pays for the narrow
+    // BN 16 tiles (15.6 vs 20.6 us, 18.6 vs 24.7 us) and for grids of more
+    // than two CTAs per SM; for BN >= 32 at <= 2 CTAs per SM the extra CTAs
+    // hide more latency than the dead half-rows cost
     const int64_t ctas = g.grid_m * g.grid_n * g.splits;
-    a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && ctas > 2 * 148 ? 1 : 0;
+    a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && (g.bn <= 16 || ctas > 2 * 148) ? 1 : 0;
   }
   const int64_t grid_y = a.pair ? (g.grid_m + 1) / 2 : g.grid_m;
   static bool nonportable = false;
