@@ -1,6 +1,8 @@
-"""Per-configuration latency of one kernel family of a population, each
-distinct configuration measured in its own measure call with >= 100
-back-to-back timed repeats (the bench's best-schedule method):
+"""Per-configuration latency of one kernel family of a population: every
+candidate of the family measured in its own measure call with >= 100
+back-to-back timed repeats (the bench's best-schedule method), the fastest
+candidate per kernel configuration reported (a candidate's latency covers all
+of its kernels, e.g. a separate pad stage before a conv):
   python scripts/family_best.py conv2d tcgen05_conv"""
 import os
 import sys
@@ -20,12 +22,14 @@ r = B200Runner(dtype="f32" if workload == "gmm512" else "bf16", min_repeats=100,
 r.set_workload(hdr["e0"])
 progs = [p["program"] for p in pop]
 plans = r.plan_programs(progs)
-seen, rows = set(), []
+best = {}
 for i, p in enumerate(plans):
-    if p["family"] != family or p["status"] != "OK" or tuple(p["cfg"]) in seen:
+    if p["family"] != family or p["status"] != "OK":
         continue
-    seen.add(tuple(p["cfg"]))
     x, = r.measure_programs([progs[i]])
-    rows.append((x["latency_ns"] / 1e3, x["status"], x["repeats"], p["cfg"]))
-for us, st, reps, cfg in sorted(rows):
-    print(f"{us:8.2f} us {flops / us / 1e6:8.1f} TF/s  {st} reps {reps} cfg {cfg}")
+    k = tuple(p["cfg"])
+    if x["status"] == "OK" and (k not in best or x["latency_ns"] < best[k][0]):
+        best[k] = (x["latency_ns"], x["repeats"], i)
+for k, (ns, reps, i) in sorted(best.items(), key=lambda kv: kv[1][0]):
+    us = ns / 1e3
+    print(f"{us:8.2f} us {flops / us / 1e6:8.1f} TF/s  reps {reps} cfg {list(k)} program #{i}")
