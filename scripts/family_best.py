@@ -23,10 +23,11 @@ r.set_workload(hdr["e0"])
 progs = [p["program"] for p in pop]
 plans = r.plan_programs(progs)
 best = {}
-for i, p in enumerate(plans):
-    if p["family"] != family or p["status"] != "OK":
-        continue
-    x, = r.measure_programs([progs[i]])
+idx = [i for i, p in enumerate(plans) if p["family"] == family and p["status"] == "OK"]
+batch = "--batch" in sys.argv  # all candidates in one measure call (as the bench's final re-measure)
+res = r.measure_programs([progs[i] for i in idx]) if batch else [r.measure_programs([progs[i]])[0] for i in idx]
+for i, x in zip(idx, res):
+    p = plans[i]
     k = tuple(p["cfg"])
     if x["status"] == "OK" and (k not in best or x["latency_ns"] < best[k][0]):
         best[k] = (x["latency_ns"], x["repeats"], i)
