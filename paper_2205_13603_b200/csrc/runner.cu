@@ -25,7 +25,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
-#include <tuple>
 #include <mutex>
 #include <memory>
 #include <string>
@@ -118,22 +117,6 @@ bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape) {
   cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// bf16 NHWC activation as 8-channel windows {8, hw, hh, 1}, no swizzle: the
-// tcgen05 conv's halo mode lands each chunk as [h][w][16 B] rows
-bool make_nhwc_halo_map(CUtensorMap* map, void* base, const int64_t* shape, int hw, int hh) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc || shape[3] % 8 != 0) return false;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(shape[3]), static_cast<cuuint64_t>(shape[2]),
-                        static_cast<cuuint64_t>(shape[1]), static_cast<cuuint64_t>(shape[0])};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(shape[3] * 2), static_cast<cuuint64_t>(shape[2] * shape[3] * 2),
-                           static_cast<cuuint64_t>(shape[1] * shape[2] * shape[3] * 2)};
-  cuuint32_t box[4] = {8, static_cast<cuuint32_t>(hw), static_cast<cuuint32_t>(hh), 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -366,16 +349,6 @@ struct ls_runner {
     if (!make_nhwc_out_map(&m, const_cast<void*>(buf), shape)) return nullptr;
     return &(tmap_o[buf] = m);
   }
-  std::map<std::tuple<const void*, int, int>, CUtensorMap> tmap_xh;  // halo windows, box {8, hw, hh, 1}
-  const CUtensorMap* map_x_halo(const void* buf, const int64_t* shape, int hw, int hh) {
-    std::lock_guard<std::mutex> lk(map_mu);
-    const auto key = std::make_tuple(buf, hw, hh);
-    auto it = tmap_xh.find(key);
-    if (it != tmap_xh.end()) return &it->second;
-    CUtensorMap m;
-    if (!make_nhwc_halo_map(&m, const_cast<void*>(buf), shape, hw, hh)) return nullptr;
-    return &(tmap_xh[key] = m);
-  }
   const CUtensorMap* map_x(const void* buf, const int64_t* shape) {
     std::lock_guard<std::mutex> lk(map_mu);
     auto it = tmap_x.find(buf);
@@ -417,12 +390,8 @@ struct ls_runner {
         const CUtensorMap* mc = p.gp->gen.ndim[stp.c_buf] == 4 && B.dtype[stp.c_buf] == 1
                                     ? map_o(B.ptr[stp.c_buf], B.shape[stp.c_buf])
                                     : nullptr;
-        int hw = 0, hh = 0;
-        const CUtensorMap* mh = tc_conv_halo_dims(stp.conv, &hw, &hh)
-                                    ? map_x_halo(B.ptr[stp.x_buf], B.shape[stp.x_buf], hw, hh)
-                                    : nullptr;
         ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, q, trace, sy, mc,
-                            mc ? B.shape[stp.c_buf] : nullptr, mh);
+                            mc ? B.shape[stp.c_buf] : nullptr);
       } else if (stp.family == F_AFFCOPY) {
         ok = launch_affcopy(stp.copy, B, dl, flag, q);
       } else if (stp.family == F_SIMTA) {

@@ -12,17 +12,6 @@
 // 2j+1 in rows 64..127 of every stage, one weight slice for both, so every
 // UMMA row is live and the grid halves.
 //
-// HALO mode (every k-tile of a split reads the same channel tile of the same
-// image -- the BASELINE 3x3 conv): the split's whole input window, (8 + taps
-// - 1)^2 pixels x 64 channels, is loaded ONCE per CTA as eight 8-channel
-// chunks [row = h * hw + w][16 B] (SWIZZLE_NONE), and the A operand of tap
-// (dh, dw) is a descriptor into that window: 8-pixel core-matrix rows are
-// consecutive window rows, the next output row is hw window rows further
-// (SBO = 16 hw bytes), the next 8 channels the next chunk (LBO).  The input
-// is read from L2 once instead of once per tap (9x less activation traffic
-// for 3x3); only the weight slices stream through the stage ring.  UMMA rows
-// 64..127 read past the window into slack and are never read back.
-//
 // Warp roles and pipeline as in tc_gemm.cu (TMA producer lane, single MMA
 // issuer, S-stage mbarrier ring, PDL).  Filter-row parts hoisted above every
 // spatial loop are split-K: the split CTAs form a cluster and reduce through
@@ -58,9 +47,7 @@ constexpr int kMaxClusterSplits = 16;
 // single producer thread ~1000 cycles of 64-bit division per k-tile).
 struct KCoord {
   int32_t c, w, h, n, kf, pad;
-  int32_t dh, dw;  // halo mode: the tap's offset inside its split's window
 };
-constexpr int kMaxHaloSplits = 16;
 
 struct TcConvArgs {
   float* c;
@@ -74,10 +61,6 @@ struct TcConvArgs {
   int tma_epi;                // modes 0/2: 128B-swizzled [64 px][32 ch] chunks -> 4-D TMA store / add-reduce
   int pair;                   // two boxes per CTA (grid y = pairs of boxes)
   int grid_m;                 // boxes (pair: the odd last pair has one)
-  int halo, hh, hw;           // halo mode: window rows / columns
-  uint32_t chunk;             // halo mode: bytes per 8-channel chunk (128-aligned)
-  uint32_t halo_bytes;        // halo mode: 8 chunks + slack for the dead UMMA rows
-  int32_t horg[kMaxHaloSplits][4];  // halo mode: window origin (h, w, c, n) of each split
   int64_t oshape[4];          // output [n][p][q][k] (decodes the box origin for the C tensor map)
 };
 
@@ -118,16 +101,15 @@ void host_add_parts(const CList& L, int64_t idx, Coord& a) {
 
 __global__ void __launch_bounds__(128, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
-               const __grid_constant__ CUtensorMap tmc, const __grid_constant__ CUtensorMap tmh,
-               const __grid_constant__ TcConvArgs a) {
+               const __grid_constant__ CUtensorMap tmc, const __grid_constant__ TcConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const int b_bytes = a.bn * 64 * 2;
-  const uint32_t a0 = base;  // A stage ring, or the halo window
-  const uint32_t b0 = base + (a.halo ? a.halo_bytes : static_cast<uint32_t>(a.stages * kStageA));
+  const uint32_t a0 = base;
+  const uint32_t b0 = base + a.stages * kStageA;
   const int red_ld = a.bn + 4;
   const uint32_t stage_end = b0 + a.stages * b_bytes;
   const int S_cl = a.mode == 1 ? a.splits : 1;
@@ -138,8 +120,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const uint32_t red_end = red + red_bytes;
   const uint32_t bars = ((stage_end > red_end ? stage_end : red_end) + 15u) & ~15u;
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
-  const uint32_t hbar = done + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
@@ -162,9 +143,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       mbar_init(empty + 8 * s, 1);
     }
     mbar_init(done, 1);
-    mbar_init(hbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.halo ? &tmh : &tmx)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmw)) : "memory");
   }
   tc_fence_before();
@@ -220,24 +200,13 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    if (a.halo) {  // the split's input window, once: eight 8-channel chunks
-      const int32_t* ho = a.horg[blockIdx.z];
-      mbar_expect_tx(hbar, static_cast<uint32_t>(8 * a.hh * a.hw * 16));
-      for (int j = 0; j < 8; ++j)
-        tma_load_4d(a0 + j * a.chunk, &tmh, hbar, static_cast<int>(o.c) + ho[2] + 8 * j,
-                    static_cast<int>(o.w) + ho[1], static_cast<int>(o.h) + ho[0], static_cast<int>(o.n) + ho[3]);
-    }
-    const uint32_t stage_bytes = (a.halo ? 0 : nbox * kLiveA) + b_bytes;
+    const uint32_t stage_bytes = nbox * kLiveA + b_bytes;
     for (int kt = 0; kt < a.kt; ++kt) {
       const int s = kt % a.stages;
       const uint32_t ph = (kt / a.stages) & 1;
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
       const KCoord k = kc[kt];
       mbar_expect_tx(full + 8 * s, stage_bytes);
-      if (a.halo) {
-        tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf, static_cast<int>(o.co), 0);
-        continue;
-      }
       tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c, static_cast<int>(o.w) + k.w,
                   static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n);
       if (nbox == 2)  // rows 64..127: the second box (8 KB = 8 swizzle atoms in)
@@ -247,27 +216,16 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
-    if (a.halo) mbar_wait(hbar, 0);
     for (int kt = 0; kt < a.kt; ++kt) {
       const int s = kt % a.stages;
       const uint32_t ph = (kt / a.stages) & 1;
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
       if (tr && kt == 0) tr[2] = gtime();
-      const uint32_t sb = b0 + s * b_bytes;
-      if (a.halo) {
-        const KCoord k = kc[kt];
-        const uint32_t sa = a0 + static_cast<uint32_t>((k.dh * a.hw + k.dw) * 16);
+      const uint32_t sa = a0 + s * kStageA, sb = b0 + s * b_bytes;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // K 16 = chunks 2kk, 2kk + 1
-          umma_bf16(tmem, sdesc_kmajor_noswizzle(sa + 2 * kk * a.chunk, a.chunk, static_cast<uint32_t>(a.hw * 16)),
-                    sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
-      } else {
-        const uint32_t sa = a0 + s * kStageA;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
-      }
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
       umma_commit(empty + 8 * s);
     }
     umma_commit(done);
@@ -403,43 +361,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
 void preload_tc_conv() { opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel)); }
 
-namespace {
-
-// the KCoord table of a conv configuration (per split, per k-tile)
-Coord kcoord(const TcConvCfg& g, int64_t sp, int64_t kt) {
-  Coord t{0, 0, 0, 0, 0, 0, 0};
-  host_add_parts(g.k_split, sp, t);
-  host_add_parts(g.k_tile, kt, t);
-  return t;
-}
-
-}  // namespace
-
-bool tc_conv_halo_dims(const TcConvCfg& g, int* hw, int* hh) {
-  if (g.splits > kMaxHaloSplits || g.splits * g.kt > kConvMaxK) return false;
-  int w0 = -1, h0 = -1;
-  for (int64_t sp = 0; sp < g.splits; ++sp) {
-    const Coord first = kcoord(g, sp, 0);
-    int64_t hmin = first.h, hmax = first.h, wmin = first.w, wmax = first.w;
-    for (int64_t kt = 0; kt < g.kt; ++kt) {
-      const Coord t = kcoord(g, sp, kt);
-      if (t.c != first.c || t.n != first.n) return false;  // one channel tile, one image per split
-      hmin = std::min(hmin, t.h); hmax = std::max(hmax, t.h);
-      wmin = std::min(wmin, t.w); wmax = std::max(wmax, t.w);
-    }
-    const int w = static_cast<int>(8 + wmax - wmin), h = static_cast<int>(8 + hmax - hmin);
-    if ((w0 >= 0 && (w != w0 || h != h0)) || w > 256 || h > 256) return false;
-    w0 = w;
-    h0 = h;
-  }
-  *hw = w0;
-  *hh = h0;
-  return w0 > 0;
-}
-
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
                     cudaStream_t st, unsigned long long* trace, uint32_t* sync, const void* tmap_c,
-                    const int64_t* oshape, const void* tmap_halo) {
+                    const int64_t* oshape) {
   static int max_dyn = -1;
   if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
@@ -464,7 +388,6 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
       k.n = static_cast<int32_t>(t.n);
       k.kf = static_cast<int32_t>(t.kf);
       k.pad = 0;
-      k.dh = k.dw = 0;
     }
   a.bn = static_cast<int>(g.bn);
   a.splits = static_cast<int>(g.splits);
@@ -501,45 +424,6 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     const int64_t ctas = g.grid_m * g.grid_n * g.splits;
     a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && (g.bn <= 16 || ctas > 2 * 148) ? 1 : 0;
   }
-  // halo mode (see the top of the file): one input window per split
-  a.halo = 0;
-  a.hh = a.hw = 0;
-  a.chunk = a.halo_bytes = 0;
-  int hw = 0, hh = 0;
-  if (tmap_halo && tc_conv_halo_dims(g, &hw, &hh)) {
-    const uint32_t chunk = static_cast<uint32_t>((hh * hw * 16 + 127) & ~127);
-    // UMMA rows 64..127 of the last chunk read up to 15 + (hh - 8) window
-    // rows past it plus the tap offset: slack of (16 + hh) * hw rows
-    const uint32_t halo_bytes = (8 * chunk + static_cast<uint32_t>((16 + hh) * hw * 16) + 1023u) & ~1023u;
-    const int64_t staged = a.tma_epi ? (g.bn / 32) * 8192 : kRows * (g.bn + 4) * 4;
-    const int64_t need = 1024 + std::max<int64_t>(halo_bytes + g.stages * g.bn * 128, staged) + 16 * g.stages + 64;
-    if (need <= g.smem_bytes) {
-      a.halo = 1;
-      a.hh = hh;
-      a.hw = hw;
-      a.chunk = chunk;
-      a.halo_bytes = halo_bytes;
-      a.pair = 0;
-      for (int64_t sp = 0; sp < g.splits; ++sp) {
-        int64_t hmin = 0, wmin = 0;
-        for (int64_t kt = 0; kt < g.kt; ++kt) {
-          const Coord t = kcoord(g, sp, kt);
-          if (kt == 0 || t.h < hmin) hmin = t.h;
-          if (kt == 0 || t.w < wmin) wmin = t.w;
-        }
-        const Coord f = kcoord(g, sp, 0);
-        a.horg[sp][0] = static_cast<int32_t>(hmin);
-        a.horg[sp][1] = static_cast<int32_t>(wmin);
-        a.horg[sp][2] = static_cast<int32_t>(f.c);
-        a.horg[sp][3] = static_cast<int32_t>(f.n);
-        for (int64_t kt = 0; kt < g.kt; ++kt) {
-          const Coord t = kcoord(g, sp, kt);
-          a.kc[sp * g.kt + kt].dh = static_cast<int32_t>(t.h - hmin);
-          a.kc[sp * g.kt + kt].dw = static_cast<int32_t>(t.w - wmin);
-        }
-      }
-    }
-  }
   const int64_t grid_y = a.pair ? (g.grid_m + 1) / 2 : g.grid_m;
   static bool nonportable = false;
   if (a.mode == 1 && g.splits > 8 && !nonportable) {
@@ -566,8 +450,7 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
   const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
   const CUtensorMap tcm = a.tma_epi ? *static_cast<const CUtensorMap*>(tmap_c) : tw;
-  const CUtensorMap thm = a.halo ? *static_cast<const CUtensorMap*>(tmap_halo) : tx;
-  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, tcm, thm, a) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, tcm, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }

@@ -9,13 +9,8 @@ namespace lsb {
 
 // tmap_x: 4-D bf16 map over the X-side buffer [n][h][w][c], box {64, 8, 8, 1};
 // tmap_w: 3-D bf16 map over the K-major weight copy [co][k_flat], box {64, bn, 1}.
-// tmap_halo: 4-D bf16 map over the same buffer, box {8, hw, hh, 1}, no
-// swizzle (halo mode, see tc_conv.cu); hw / hh from tc_conv_halo_dims.
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& cfg, bool pdl,
                     cudaStream_t st, unsigned long long* trace = nullptr, uint32_t* sync = nullptr,
-                    const void* tmap_c = nullptr, const int64_t* oshape = nullptr, const void* tmap_halo = nullptr);
-// Window extents of the halo mode: every k-tile of a split reads the same
-// channel tile of the same image (false otherwise).
-bool tc_conv_halo_dims(const TcConvCfg& cfg, int* hw, int* hh);
+                    const void* tmap_c = nullptr, const int64_t* oshape = nullptr);
 
 }  // namespace lsb
