@@ -173,6 +173,25 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
   plan.status = P_OK;
   bool all_serial = true;
   for (const Part& q : parts) all_serial &= q.kind == Kind::Serial;
+  // traced pipeline depth (tensor_core.py, pipeline=True): the only
+  // non-serial loop is an unrolled K part directly above the tile's M part;
+  // it is a k-tile loop like any other, its extent the stage count
+  int64_t traced_stages = 0;
+  {
+    int nonserial = 0;
+    size_t at = 0;
+    for (size_t i = 0; i < parts.size(); ++i)
+      if (parts[i].kind != Kind::Serial) {
+        ++nonserial;
+        at = i;
+      }
+    if (nonserial == 1 && lim.bf16 && parts[at].kind == Kind::Unrolled && parts[at].role == R_K &&
+        at + 1 < parts.size() && parts[at + 1].role == R_M) {
+      traced_stages = parts[at].extent;
+      parts[at].kind = Kind::Serial;
+      all_serial = true;
+    }
+  }
 
   if (!all_serial) {
     // LOOPNEST: parallel outermost loop -> threads; everything else in order
@@ -238,11 +257,14 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
         if (before_spatial) t.splits *= merged[i].extent;
         else t.kt *= merged[i].extent;
       }
-      // stage count: as many k-tiles as fit in shared memory (<= 8)
+      // stage count: the traced pipeline depth, or as many k-tiles as fit in
+      // shared memory (<= 8)
       const int64_t tiles = t.batch * t.grid_m * t.grid_n;
       const TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles);
       const int64_t avail = lim.max_smem - 1024 - 256;
-      t.stages = std::min<int64_t>({t.kt, std::max<int64_t>(1, avail / g0.stage_bytes), 8});
+      const int64_t fit = std::max<int64_t>(1, avail / g0.stage_bytes);
+      t.stages = traced_stages ? std::min(traced_stages, t.kt) : std::min<int64_t>({t.kt, fit, 8});
+      if (traced_stages > fit) return illegal(plan, "traced pipeline depth above shared memory");
       const TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles);
       plan.needs_zero = g.mode == 3;
       t.smem_bytes = g.smem;
@@ -257,6 +279,8 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       return plan;
     }
   }
+
+  if (traced_stages) return unsupported("unrolled k-tile loop outside a tcgen05 tile");
 
   // ---- SIMT: grid / threads / registers per spatial axis ------------------
   plan.family = F_SIMT;

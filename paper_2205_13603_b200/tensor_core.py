@@ -23,6 +23,10 @@ Decisions (all traced, so search and mutation see them):
     the hardware validator.
   * K: ``split(k, [K/64, 64])`` then ``sample_perfect_tile(k_hi, 2)`` gives
     (split-K ways, k-tiles per split); 64 bf16 = one 128-byte swizzle row.
+  * pipeline depth (``use_tensor_core(pipeline=True)``): the k-tiles of a
+    split are split once more, ``sample_perfect_tile(kt, 2)`` -> (kt / S, S),
+    and the inner part is ``unroll``-ed; the instantiator reads S as the
+    number of shared-memory stages in flight (ILLEGAL above what fits).
 """
 
 from __future__ import annotations
@@ -113,6 +117,9 @@ def _module_class():
     class _UseTensorCore(TransformationModule):
         name = "use_tensor_core"
 
+        def __init__(self, pipeline: bool = False):
+            self.pipeline = pipeline
+
         def applicability(self, state, block):
             if not state.block_exists(block):
                 return False
@@ -167,7 +174,12 @@ def _module_class():
             k_hi, k64 = state.split(by_var[kv], [ext[kv] // BLOCK_K, BLOCK_K])
             ks, kt = state.split(k_hi, state.sample_perfect_tile(k_hi, 2))
             batch = [by_var[b] for b in roles["batch"]]
-            state.reorder([ks] + batch + [m0, n0, kt, m1, n1, n16, k64])
+            if self.pipeline:  # traced stage count: the unrolled inner k-tile part
+                kto, kst = state.split(kt, state.sample_perfect_tile(kt, 2))
+                state.unroll(kst)
+                state.reorder([ks] + batch + [m0, n0, kto, kst, m1, n1, n16, k64])
+            else:
+                state.reorder([ks] + batch + [m0, n0, kt, m1, n1, n16, k64])
 
     return _UseTensorCore
 
@@ -175,12 +187,12 @@ def _module_class():
 _CLS = None
 
 
-def use_tensor_core():
+def use_tensor_core(pipeline: bool = False):
     """Factory mirroring the reference's module factories (`src/spaces.py:311`)."""
     global _CLS
     if _CLS is None:
         _CLS = _module_class()
-    return _CLS()
+    return _CLS(pipeline=pipeline)
 
 
 def space_from_config(doc: dict):
@@ -195,17 +207,20 @@ def space_from_config(doc: dict):
             raise ValueError(f"modules[{i}]: expected a single-key object")
         kind = next(iter(entry))
         if kind == "tensor_core":
-            modules.append(use_tensor_core())
+            opts = entry[kind] or {}
+            modules.append(use_tensor_core(pipeline=bool(opts.get("pipeline", False))))
         else:
             modules.append(ls.space_from_config({"modules": [entry]}).modules[0])
     return ls.compose(modules)
 
 
-def b200_space_config() -> dict:
-    """Default space + the tcgen05 module (the BERT dense/bmm search space)."""
+def b200_space_config(pipeline: bool = False) -> dict:
+    """Default space + the tcgen05 module (the BERT dense/bmm search space);
+    ``pipeline`` adds the traced stage count."""
     return {"modules": [{"mlt": {"structure": "SSRSR"}}, {"auto_inline": {}},
-                        {"pvu": {"widths": [4, 8]}}, {"tensor_core": {}}]}
+                        {"pvu": {"widths": [4, 8]}},
+                        {"tensor_core": {"pipeline": True} if pipeline else {}}]}
 
 
-def b200_space():
-    return space_from_config(b200_space_config())
+def b200_space(pipeline: bool = False):
+    return space_from_config(b200_space_config(pipeline))

@@ -381,3 +381,26 @@ def test_simt_wide_register_tiles_and_chunked_k_tiles_exact():
             assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
     assert ok >= 6
     r.close()
+
+
+def test_traced_pipeline_depth_candidates_exact():
+    # tcgen05 candidates of the pipelined b200 space (the unrolled inner
+    # k-tile part = shared-memory stages in flight) are bit-exact for every
+    # traced depth
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.tensor_core import b200_space
+    ls = loopsched()
+    e0 = ls.ir.serialize(ls.gmm(128, 768, 3072))
+    progs = [ls.ir.serialize(p) for p, _ in
+             ls.spaces.sample_traces(ls.ir.deserialize(e0), b200_space(pipeline=True), 96, seed=11)]
+    r = make_runner("bf16", timeout_ms=50.0)
+    r.set_workload(e0, seed=0)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 0)).values()))
+    plans = r.plan_programs(progs)
+    tc = [i for i, p in enumerate(plans) if p["family"] == "tcgen05" and p["status"] == "OK"]
+    assert len({plans[i]["cfg"][6] for i in tc}) >= 3
+    for i in tc:
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] == "OK" and res["mismatches"] == 0, res
+        assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
+    r.close()

@@ -122,3 +122,40 @@ def test_fused_pvu_schedules_fall_back_to_the_general_families():
     c = Counter((r["family"], r["status"]) for r in res)
     assert c[("nestgen", "OK")] > 0
     assert not [r for r in res if r["status"] == "UNSUPPORTED"]
+
+
+@pytest.mark.skipif(not __import__("conftest").has_reference(), reason="needs the reference package")
+def test_traced_pipeline_depth_sets_tcgen05_stages():
+    # use_tensor_core(pipeline=True): the unrolled inner k-tile part is the
+    # stage count of the tcgen05 candidate (ILLEGAL above what fits)
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.tensor_core import b200_space
+    ls = loopsched()
+    e0 = ls.gmm(128, 768, 3072)
+    progs = [ls.ir.serialize(p) for p, _ in ls.spaces.sample_traces(e0, b200_space(pipeline=True), 96, seed=11)]
+    res = plan(ls.ir.serialize(e0), progs)
+
+    def unrolled(text):
+        out = []
+
+        def walk(stmts):
+            for st in stmts:
+                if "loop" in st:
+                    if st["loop"]["kind"] == "unrolled":
+                        out.append(st["loop"]["extent"])
+                    walk(st["loop"]["body"])
+        walk(json.loads(text)["root"])
+        return out
+
+    tc = [(p, r) for p, r in zip(progs, res) if r["family"] == "tcgen05"]
+    assert len(tc) >= 8
+    depths = set()
+    for p, r in tc:
+        u = unrolled(p)
+        assert len(u) == 1
+        if r["status"] == "OK":
+            assert r["cfg"][6] == u[0], (r["cfg"], u)   # cfg[6] = stages
+            depths.add(u[0])
+        else:
+            assert r["status"] == "ILLEGAL"
+    assert len(depths) >= 3
