@@ -205,6 +205,10 @@ ls_status ls_replayer_hash(ls_replayer* r, uint64_t* out); /* ir.structural_hash
 ls_status ls_replay_batch(ls_replayer* r, const char* const* traces, const size_t* lens, int n,
                           ls_replay_result* out);
 void ls_replay_free(ls_replay_result* res, int n);
+/* replay(e0, t, mode="resample", seed) (src/trace.py:163-188): the samplers
+ * draw fresh decisions from CPython's random.Random(seed), bit-exact (the
+ * fresh candidates of evolve, src/search.py:149-159); same result form. */
+ls_status ls_replay_resample(ls_replayer* r, const char* trace, size_t len, uint64_t seed, ls_replay_result* out);
 void ls_replayer_destroy(ls_replayer* r);
 /* Look-ahead: every single-decision neighbour of each
  * member trace -- exactly the traces `mutate` (src/trace.py:287-309) can

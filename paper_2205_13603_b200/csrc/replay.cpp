@@ -976,6 +976,81 @@ const IntrInfo* intrinsic(const std::string& n) {
   return nullptr;
 }
 
+void factorizations(int64_t extent, int64_t n, std::vector<int64_t>& cur, std::vector<std::vector<int64_t>>* out);
+
+// CPython's random.Random (Modules/_randommodule.c, Lib/random.py): MT19937
+// seeded by init_by_array over the 32-bit words of |seed|, getrandbits(k) =
+// the top k bits of one output, randrange(n) = _randbelow_with_getrandbits,
+// random() = 53 bits from two outputs -- bit-exact, so a resampled replay
+// draws the decisions the reference draws for the same seed.
+class PyRandom {
+ public:
+  explicit PyRandom(uint64_t seed) {
+    uint32_t key[2] = {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)};
+    init_by_array(key, key[1] ? 2 : 1);
+  }
+  uint32_t next() {
+    if (idx_ >= 624) twist();
+    uint32_t y = mt_[idx_++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    y ^= y >> 18;
+    return y;
+  }
+  uint32_t getrandbits(int k) { return k <= 0 ? 0u : next() >> (32 - k); }
+  int64_t randbelow(int64_t n) {  // n >= 1, n < 2**32
+    int k = 0;
+    while ((int64_t{1} << k) <= n) ++k;  // n.bit_length()
+    int64_t r = getrandbits(k);
+    while (r >= n) r = getrandbits(k);
+    return r;
+  }
+  double random() {
+    const uint32_t a = next() >> 5, b = next() >> 6;
+    return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+  }
+
+ private:
+  void init_genrand(uint32_t s) {
+    mt_[0] = s;
+    for (int i = 1; i < 624; ++i) mt_[i] = 1812433253u * (mt_[i - 1] ^ (mt_[i - 1] >> 30)) + static_cast<uint32_t>(i);
+    idx_ = 624;
+  }
+  void init_by_array(const uint32_t* key, int len) {
+    init_genrand(19650218u);
+    int i = 1, j = 0;
+    for (int k = 624 > len ? 624 : len; k; --k) {
+      mt_[i] = (mt_[i] ^ ((mt_[i - 1] ^ (mt_[i - 1] >> 30)) * 1664525u)) + key[j] + static_cast<uint32_t>(j);
+      ++i;
+      ++j;
+      if (i >= 624) {
+        mt_[0] = mt_[623];
+        i = 1;
+      }
+      if (j >= len) j = 0;
+    }
+    for (int k = 623; k; --k) {
+      mt_[i] = (mt_[i] ^ ((mt_[i - 1] ^ (mt_[i - 1] >> 30)) * 1566083941u)) - static_cast<uint32_t>(i);
+      ++i;
+      if (i >= 624) {
+        mt_[0] = mt_[623];
+        i = 1;
+      }
+    }
+    mt_[0] = 0x80000000u;
+  }
+  void twist() {
+    for (int i = 0; i < 624; ++i) {
+      const uint32_t y = (mt_[i] & 0x80000000u) | (mt_[(i + 1) % 624] & 0x7fffffffu);
+      mt_[i] = mt_[(i + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    }
+    idx_ = 0;
+  }
+  uint32_t mt_[624];
+  int idx_ = 624;
+};
+
 enum RefKind : uint8_t { RK_BLOCK, RK_LOOP, RK_RV };
 enum LocKind : uint8_t { L_ROOT, L_INLINE, L_LOOP };
 struct Ref {
@@ -1070,6 +1145,9 @@ class State {
   // e0_vars: the loop variables of the workload program, the only names a
   // fresh "x<n>" variable can collide with
   State(Prog p, const std::set<std::string>* e0_vars) : prog(std::move(p)), e0_vars_(e0_vars) {}
+  // resample mode (replay(..., mode="resample", seed)): the samplers draw
+  // from this generator instead of following the recorded decisions
+  std::shared_ptr<PyRandom> rng;
 
   Ref* ref_at(int i) { return &refs_[static_cast<size_t>(i)]; }
   Ref* new_ref(RefKind k, std::string payload) {
@@ -1926,11 +2004,19 @@ class State {
     const int64_t n = nval->i;
     if (n < 1) sched_err("sample_perfect_tile: n must be >= 1");
     auto [path, node] = resolve_loop(loop);
-    if (!decision || decision->t != Value::Arr) defer("tile decision");
     std::vector<int64_t> tile;
-    for (const Value& x : decision->a) {
-      if (x.t != Value::Int || x.big) defer("non-integer tile decision");
-      tile.push_back(x.i);
+    if (rng) {  // domain[_draw_index(len(domain))], the lexicographic domain of ordered_factorizations
+      if (n > 8 || node->extent < 1) defer("tile domain");
+      std::vector<std::vector<int64_t>> dom;
+      std::vector<int64_t> cur;
+      factorizations(node->extent, n, cur, &dom);
+      tile = dom[static_cast<size_t>(rng->randbelow(static_cast<int64_t>(dom.size())))];
+    } else {
+      if (!decision || decision->t != Value::Arr) defer("tile decision");
+      for (const Value& x : decision->a) {
+        if (x.t != Value::Int || x.big) defer("non-integer tile decision");
+        tile.push_back(x.i);
+      }
     }
     bool bad = static_cast<int64_t>(tile.size()) != n;
     for (int64_t f : tile) bad |= f < 1;
@@ -1971,8 +2057,22 @@ class State {
     double total = 0;  // float(sum(probs)): Python sums left to right from int 0
     for (double x : w) total += x;
     if (!(total > 0)) sched_err("sample_categorical: all-zero weights");
-    if (!decision || decision->t != Value::Int || decision->big) defer("categorical decision");
-    const int64_t idx = decision->i;
+    int64_t idx;
+    if (rng) {  // _draw_index with weights (src/schedule.py:174-186)
+      const double r = rng->random() * total;
+      double acc = 0.0;
+      idx = static_cast<int64_t>(w.size()) - 1;
+      for (size_t i = 0; i < w.size(); ++i) {
+        acc += w[i];
+        if (r < acc) {
+          idx = static_cast<int64_t>(i);
+          break;
+        }
+      }
+    } else {
+      if (!decision || decision->t != Value::Int || decision->big) defer("categorical decision");
+      idx = decision->i;
+    }
     if (!(0 <= idx && idx < static_cast<int64_t>(cands->a.size())) || w[static_cast<size_t>(idx)] <= 0)
       sched_err("sample_categorical: decision " + std::to_string(idx) + " out of domain");
     Ref* r = new_ref(RK_RV, "");
@@ -1999,8 +2099,13 @@ class State {
     if (!cand) sched_err("sample_compute_location: block " + bs->name + " has no counterpart");
     const bool can_inline = inline_mode(*bs).has_value();
     const int64_t size = 1 + (can_inline ? 1 : 0) + static_cast<int64_t>(cand->loops.size());
-    if (!decision || decision->t != Value::Int || decision->big) defer("location decision");
-    const int64_t idx = decision->i;
+    int64_t idx;
+    if (rng) {
+      idx = rng->randbelow(size);
+    } else {
+      if (!decision || decision->t != Value::Int || decision->big) defer("location decision");
+      idx = decision->i;
+    }
     if (!(0 <= idx && idx < size))
       sched_err("sample_compute_location: decision " + std::to_string(idx) + " outside domain of size " +
                 std::to_string(size));
@@ -2238,15 +2343,18 @@ void step(State& st, Env& env, const Value& ins, int index) {
     } else if (op == "tensorize") {
       st.tensorize(arg(0), attrs->get("intrinsic"));
     } else if (op == "sample_perfect_tile") {
-      if (!decision || decision->t != Value::Obj) defer("decision");
-      bind_outputs(ins, st.sample_perfect_tile(arg(0), attrs->get("n"), decision->get("tile")), env, index, op);
+      if (!st.rng && (!decision || decision->t != Value::Obj)) defer("decision");
+      bind_outputs(ins, st.sample_perfect_tile(arg(0), attrs->get("n"), st.rng ? nullptr : decision->get("tile")),
+                   env, index, op);
     } else if (op == "sample_categorical") {
-      if (!decision || decision->t != Value::Obj) defer("decision");
-      bind_outputs(ins, {st.sample_categorical(attrs->get("candidates"), attrs->get("probs"), decision->get("index"))},
+      if (!st.rng && (!decision || decision->t != Value::Obj)) defer("decision");
+      bind_outputs(ins, {st.sample_categorical(attrs->get("candidates"), attrs->get("probs"),
+                                               st.rng ? nullptr : decision->get("index"))},
                    env, index, op);
     } else if (op == "sample_compute_location") {
-      if (!decision || decision->t != Value::Obj) defer("decision");
-      bind_outputs(ins, {st.sample_compute_location(arg(0), decision->get("index"))}, env, index, op);
+      if (!st.rng && (!decision || decision->t != Value::Obj)) defer("decision");
+      bind_outputs(ins, {st.sample_compute_location(arg(0), st.rng ? nullptr : decision->get("index"))}, env, index,
+                   op);
     } else {
       sched_err("unknown instruction op " + pj::py_repr(op));
     }
@@ -2279,7 +2387,7 @@ Outcome rejected(const ReplayErr& e) {
   return out;
 }
 
-Outcome replay_one(const Workload& w, std::string_view text) {
+Outcome replay_one(const Workload& w, std::string_view text, const uint64_t* resample_seed = nullptr) {
   Parsed P = parse_trace(text);
   Outcome out;
   if (!P.err.empty()) {
@@ -2289,6 +2397,7 @@ Outcome replay_one(const Workload& w, std::string_view text) {
   try {
     check_workload_hash(w, P);
     State st(local_e0(w), &w.loop_vars);
+    if (resample_seed) st.rng = std::make_shared<PyRandom>(*resample_seed);
     Env env;
     for (int index = 0; index < static_cast<int>(P.instrs.size()); ++index)
       step(st, env, P.instrs[static_cast<size_t>(index)], index);
@@ -2517,6 +2626,21 @@ void ls_replay_free(ls_replay_result* res, int n) {
     std::free(res[i].reason);
     res[i].program = res[i].trace = res[i].reason = nullptr;
   }
+}
+
+ls_status ls_replay_resample(ls_replayer* r, const char* trace, size_t len, uint64_t seed, ls_replay_result* out) {
+  if (!r || !trace || !out) {
+    set_error("ls_replay_resample: bad arguments");
+    return LS_ERR_ARG;
+  }
+  rp::Outcome o = rp::replay_one(r->w, std::string_view(trace, len), &seed);
+  out->status = o.status;
+  out->index = o.index;
+  out->hash = o.hash;
+  out->program = o.status == LS_REPLAY_ACCEPTED ? rp::dup_cstr(o.program) : nullptr;
+  out->trace = o.status == LS_REPLAY_ACCEPTED ? rp::dup_cstr(o.trace) : nullptr;
+  out->reason = o.status != LS_REPLAY_ACCEPTED ? rp::dup_cstr(o.reason) : nullptr;
+  return LS_OK;
 }
 
 ls_status ls_program_hash(const char* program, size_t len, uint64_t* out) {

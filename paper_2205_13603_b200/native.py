@@ -109,6 +109,8 @@ EXPORTS = {
     "ls_replay_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),
                                        ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
                                        ctypes.POINTER(ReplayResultC)]),
+    "ls_replay_resample": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64,
+                                          ctypes.POINTER(ReplayResultC)]),
     "ls_replay_free": (None, [ctypes.POINTER(ReplayResultC), ctypes.c_int]),
     "ls_replayer_destroy": (None, [ctypes.c_void_p]),
     "ls_replay_neighbours": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_char_p),

@@ -194,6 +194,16 @@ def _lookahead_validator():
     return v if v is not None and v.lookahead else None
 
 
+def _d_replay(e0, t, mode="follow", seed=0):
+    # the resampled replays of `_fresh_candidate` (src/search.py:149-159)
+    # for this block's workload go native; everything else to the reference
+    cur = _current()
+    v = cur.validator if cur is not None else None
+    if mode == "resample" and v is not None and e0 is v.e0:
+        return v.resample(t, seed)
+    return _originals[8](e0, t, mode, seed)
+
+
 def _d_evolve(*args, **kw):
     v = kw.get("validator", args[5] if len(args) > 5 else None)
     if v is not None and getattr(v, "lookahead", False):
@@ -250,9 +260,9 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
         if _install_depth == 0:
             vcls = S._Validator
             _originals = (S._measure_batch, S.simulate_latency, S.featurize, vcls._predict, vcls,
-                          S.evolve, S.mutate, S.mh_accept)
+                          S.evolve, S.mutate, S.mh_accept, S.replay)
             S._measure_batch, S.simulate_latency, S.featurize = _d_measure, _d_simulate, _d_featurize
-            S.evolve, S.mutate, S.mh_accept = _d_evolve, _d_mutate, _d_mh_accept
+            S.evolve, S.mutate, S.mh_accept, S.replay = _d_evolve, _d_mutate, _d_mh_accept, _d_replay
             vcls._predict = _d_predict
             _d_validator._ls_dispatch = True
             _d_validator._ls_base = vcls
@@ -272,7 +282,7 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
                 vcls = _originals[4]
                 S._measure_batch, S.simulate_latency, S.featurize, vcls._predict = _originals[:4]
                 S._Validator = vcls
-                S.evolve, S.mutate, S.mh_accept = _originals[5:8]
+                S.evolve, S.mutate, S.mh_accept, S.replay = _originals[5:9]
                 _originals = None
 
 

@@ -65,6 +65,20 @@ class NativeReplayer:
         self._L.ls_replay_free(res, n)
         return out
 
+    def resample(self, key: str, seed: int):
+        """``replay(e0, t, mode="resample", seed)`` of a serialized trace:
+        (status, index, hash, program_text, trace_text, reason)."""
+        res = native.ReplayResultC()
+        b = key.encode()
+        native.check(self._L.ls_replay_resample(self._h, b, len(b), seed, ctypes.byref(res)), "ls_replay_resample")
+        sa = ctypes.string_at
+        if res.status == ACCEPTED:
+            out = (res.status, res.index, res.hash, sa(res.program).decode(), sa(res.trace).decode(), None)
+        else:
+            out = (res.status, res.index, 0, None, None, sa(res.reason).decode() if res.reason else "")
+        self._L.ls_replay_free(ctypes.byref(res), 1)
+        return out
+
     def neighbours(self, member_keys):
         """Replay every single-decision neighbour of each member key not
         expanded before; returns ([(hash, program_text)] for structural
@@ -245,6 +259,8 @@ def native_validator_class():
                 self._building = False
                 self._last = None
                 self._lazies = []
+                self._keys = {}          # id(trace) -> (trace, serialize_trace(trace)) of space traces
+                self._orig_replay = ls.trace.replay
                 self.expansions = 0
                 self.neighbours = 0       # replayed by the look-ahead
                 self.prefetched = 0       # programs featurized ahead
@@ -306,19 +322,41 @@ def native_validator_class():
                     return self._note(base.candidate(self, t, model))
                 return self._note(self._store_native(key, self._trace(key, norm, t), self._lazy(prog), h, model))
 
+            def resample(self, t, seed):
+                """``replay(e0, t, "resample", seed)`` (`src/trace.py:163-198`)
+                natively: the fresh candidates of `_fresh_candidate`
+                (`src/search.py:149-159`)."""
+                key = self._keys.get(id(t))
+                if key is None or key[0] is not t:
+                    key = (t, ls.trace.serialize_trace(t))
+                    self._keys[id(t)] = key
+                st, idx, h, prog, norm, reason = self._rp.resample(key[1], seed)
+                self.native_calls += 1
+                if st == REJECTED:
+                    raise ls.trace.ReplayError(idx, reason)
+                if st == DEFER:
+                    self.deferred += 1
+                    return self._orig_replay(self.e0, t, mode="resample", seed=seed)
+                program = self._lazy(prog)
+                object.__setattr__(program, "_ls_hash", h)
+                return program, self._trace(key[1], norm, t)
+
             def from_replay(self, t, program, model):
                 # a fresh (resampled) candidate: with the look-ahead its
                 # features are computed lazily, all pending ones in one K7
                 # batch on first use (evolve reads no feature or prediction
                 # until the population is complete)
-                if not self.lookahead:
+                native_h = getattr(program, "_ls_hash", None)
+                if not self.lookahead and native_h is None:
                     return self._note(base.from_replay(self, t, program, model))
-                key = ls.trace.serialize_trace(t)
+                key = getattr(t, "_ls_key", None) or ls.trace.serialize_trace(t)
                 cand = self.cache.get(key)
                 if cand is not None:
                     return self._note(self._revive(cand, model))
-                text = ls.ir.serialize(program)
-                h = program_hash(text)
+                text = getattr(program, "_ls_text", None) or ls.ir.serialize(program)
+                h = native_h if native_h is not None else program_hash(text)
+                if not self.lookahead:
+                    return self._note(self._store_native(key, t, program, h, model))
                 if h in self.features_by_hash:
                     return self._note(self._store_native(key, t, program, h, model))
                 lazy = _lazy_candidate_class()(t, program, h, self, model, text)

@@ -128,3 +128,33 @@ def test_lookahead_prefetch_keeps_the_tune_byte_identical():
     a = json.dumps(ref.to_json(timestamp=False), sort_keys=True)
     b = json.dumps(nat.to_json(timestamp=False), sort_keys=True)
     assert a == b
+
+
+@needs_reference
+@pytest.mark.parametrize("name", ["bert_ffn", "conv2d", "gmm512"])
+def test_native_resample_equals_reference_resample(name):
+    # replay(e0, t, mode="resample", seed): the native samplers draw from a
+    # bit-exact port of CPython's random.Random(seed), so program, hash and
+    # re-recorded trace equal the reference's for every seed
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.replay import ACCEPTED, REJECTED, NativeReplayer
+    ls = loopsched()
+    hdr, rows = load_replay(name)
+    e0 = ls.ir.deserialize(hdr["e0"])
+    rp = NativeReplayer(hdr["e0"])
+    n = 0
+    for k, r in enumerate(rows[:24]):
+        t = ls.trace.deserialize_trace(r["trace"])
+        key = ls.trace.serialize_trace(t)
+        for seed in (0, 1, 12345, 2 ** 40 + k, 2 ** 62 - 1 - k):
+            st, idx, h, prog, norm, reason = rp.resample(key, seed)
+            try:
+                p, nt = ls.trace.replay(e0, t, mode="resample", seed=seed)
+            except ls.trace.ReplayError as exc:
+                assert st == REJECTED and (reason, idx) == (exc.reason, exc.index)
+                continue
+            assert st == ACCEPTED
+            assert prog == ls.ir.serialize(p) and h == ls.ir.structural_hash(p)
+            assert norm == ls.trace.serialize_trace(nt)
+            n += 1
+    assert n >= 60
