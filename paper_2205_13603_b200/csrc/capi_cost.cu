@@ -220,52 +220,41 @@ namespace {
 struct Workspace {
   std::mutex mu;
   cudaStream_t stream = nullptr;
-  int64_t *blobs = nullptr, *off = nullptr, *num = nullptr, *den = nullptr;
-  double *feats = nullptr, *pred = nullptr;
-  int32_t* status = nullptr;
-  size_t cap_words = 0, cap_n = 0;
-  // pinned host staging: blob words + offsets in, results out (pageable
-  // copies go through the driver's own staging buffer, several x slower)
-  int64_t* h_in = nullptr;   // [cap_n + 1 offsets][cap_words blob words]
-  uint8_t* h_out = nullptr;  // num | den | feats | pred | status, cap_n each
-  size_t h_in_cap = 0, h_out_cap = 0;
+  // one device block in ([n + 1 offsets][blob words]) and one out
+  // ([num n][den n][feats 9n][pred n][status n int32]), laid out per call
+  // exactly like the pinned host staging, so a call is one H2D copy, the
+  // kernel and one D2H copy (the search calls this once per new program)
+  int64_t* d_in = nullptr;
+  uint8_t* d_out = nullptr;
+  int64_t* h_in = nullptr;
+  uint8_t* h_out = nullptr;
+  size_t cap_in = 0, cap_out = 0;  // words / bytes
 };
 Workspace g_ws[64];
 
-ls_status grow(Workspace& w, size_t words, size_t n) {
+inline size_t out_bytes(size_t n) { return n * (8 + 8 + 72 + 8 + 4); }
+
+ls_status grow(Workspace& w, size_t in_words, size_t n) {
   if (!w.stream) LSB_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
-  if (words > w.cap_words) {
-    cudaFree(w.blobs);
-    w.blobs = nullptr;
-    size_t c = std::max(words, 2 * w.cap_words);
-    LSB_CUDA(cudaMalloc(&w.blobs, c * 8));
-    w.cap_words = c;
-  }
-  if (n > w.cap_n) {
-    cudaFree(w.off); cudaFree(w.num); cudaFree(w.den); cudaFree(w.feats); cudaFree(w.pred); cudaFree(w.status);
-    w.off = w.num = w.den = nullptr; w.feats = w.pred = nullptr; w.status = nullptr;
-    size_t c = std::max(n, 2 * w.cap_n);
-    LSB_CUDA(cudaMalloc(&w.off, (c + 1) * 8));
-    LSB_CUDA(cudaMalloc(&w.num, c * 8));
-    LSB_CUDA(cudaMalloc(&w.den, c * 8));
-    LSB_CUDA(cudaMalloc(&w.feats, c * 9 * 8));
-    LSB_CUDA(cudaMalloc(&w.pred, c * 8));
-    LSB_CUDA(cudaMalloc(&w.status, c * 4));
-    w.cap_n = c;
-  }
-  const size_t in_words = w.cap_n + 1 + w.cap_words;
-  if (in_words > w.h_in_cap) {
+  if (in_words > w.cap_in) {
+    cudaFree(w.d_in);
     cudaFreeHost(w.h_in);
+    w.d_in = nullptr;
     w.h_in = nullptr;
-    LSB_CUDA(cudaMallocHost(&w.h_in, in_words * 8));
-    w.h_in_cap = in_words;
+    const size_t c = std::max(in_words, 2 * w.cap_in);
+    LSB_CUDA(cudaMalloc(&w.d_in, c * 8));
+    LSB_CUDA(cudaMallocHost(&w.h_in, c * 8));
+    w.cap_in = c;
   }
-  const size_t out_bytes = w.cap_n * (8 + 8 + 72 + 8 + 4);
-  if (out_bytes > w.h_out_cap) {
+  if (out_bytes(n) > w.cap_out) {
+    cudaFree(w.d_out);
     cudaFreeHost(w.h_out);
+    w.d_out = nullptr;
     w.h_out = nullptr;
-    LSB_CUDA(cudaMallocHost(&w.h_out, out_bytes));
-    w.h_out_cap = out_bytes;
+    const size_t c = std::max(out_bytes(n), 2 * w.cap_out);
+    LSB_CUDA(cudaMalloc(&w.d_out, c));
+    LSB_CUDA(cudaMallocHost(&w.h_out, c));
+    w.cap_out = c;
   }
   return LS_OK;
 }
@@ -306,7 +295,7 @@ ls_status ls_analyze_batch(int device, const char* const* programs, const size_t
 
   Workspace& w = g_ws[device];
   std::lock_guard<std::mutex> lock(w.mu);
-  if ((st = grow(w, words, nn)) != LS_OK) return st;
+  if ((st = grow(w, nn + 1 + words, nn)) != LS_OK) return st;
   // offsets then the blobs, contiguous in pinned memory: one DMA
   int64_t* hin = w.h_in;
   std::copy(offsets.begin(), offsets.end(), hin);
@@ -314,24 +303,23 @@ ls_status ls_analyze_batch(int device, const char* const* programs, const size_t
   parallel_for(n, [&](int i) {
     std::copy(blobs[static_cast<size_t>(i)].begin(), blobs[static_cast<size_t>(i)].end(), hblob + offsets[i]);
   });
-  LSB_CUDA(cudaMemcpyAsync(w.off, hin, (nn + 1) * 8, cudaMemcpyHostToDevice, w.stream));
-  LSB_CUDA(cudaMemcpyAsync(w.blobs, hblob, words * 8, cudaMemcpyHostToDevice, w.stream));
+  LSB_CUDA(cudaMemcpyAsync(w.d_in, hin, (nn + 1 + words) * 8, cudaMemcpyHostToDevice, w.stream));
+  int64_t* d_num = reinterpret_cast<int64_t*>(w.d_out);
+  int64_t* d_den = d_num + nn;
+  double* d_feats = reinterpret_cast<double*>(d_den + nn);
+  double* d_pred = d_feats + 9 * nn;
+  int32_t* d_status = reinterpret_cast<int32_t*>(d_pred + nn);
   int flags = (num || den ? 1 : 0) | (feats ? 2 : 0) | (pred && model ? 4 : 0);
-  launch_analyze(w.blobs, w.off, n, to_dspec(spec), to_dmodel(model), flags, w.num, w.den, w.feats, w.pred,
-                 w.status, w.stream);
+  launch_analyze(w.d_in + nn + 1, w.d_in, n, to_dspec(spec), to_dmodel(model), flags, d_num, d_den, d_feats,
+                 d_pred, d_status, w.stream);
   LSB_CUDA(cudaGetLastError());
-  uint8_t* ho = w.h_out;
-  int64_t* o_num = reinterpret_cast<int64_t*>(ho);
-  int64_t* o_den = o_num + w.cap_n;
-  double* o_feats = reinterpret_cast<double*>(o_den + w.cap_n);
-  double* o_pred = o_feats + 9 * w.cap_n;
-  int32_t* o_status = reinterpret_cast<int32_t*>(o_pred + w.cap_n);
-  if (num) LSB_CUDA(cudaMemcpyAsync(o_num, w.num, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (den) LSB_CUDA(cudaMemcpyAsync(o_den, w.den, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (feats) LSB_CUDA(cudaMemcpyAsync(o_feats, w.feats, nn * 72, cudaMemcpyDeviceToHost, w.stream));
-  if (pred && model) LSB_CUDA(cudaMemcpyAsync(o_pred, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
-  if (status) LSB_CUDA(cudaMemcpyAsync(o_status, w.status, nn * 4, cudaMemcpyDeviceToHost, w.stream));
+  LSB_CUDA(cudaMemcpyAsync(w.h_out, w.d_out, out_bytes(nn), cudaMemcpyDeviceToHost, w.stream));
   LSB_CUDA(cudaStreamSynchronize(w.stream));
+  int64_t* o_num = reinterpret_cast<int64_t*>(w.h_out);
+  int64_t* o_den = o_num + nn;
+  double* o_feats = reinterpret_cast<double*>(o_den + nn);
+  double* o_pred = o_feats + 9 * nn;
+  int32_t* o_status = reinterpret_cast<int32_t*>(o_pred + nn);
   if (num) std::memcpy(num, o_num, nn * 8);
   if (den) std::memcpy(den, o_den, nn * 8);
   if (feats) std::memcpy(feats, o_feats, nn * 72);
@@ -372,12 +360,14 @@ ls_status ls_score_batch(int device, const double* feats, int n, const ls_linear
   }
   Workspace& w = g_ws[device];
   std::lock_guard<std::mutex> lock(w.mu);
-  if ((st = grow(w, 1, static_cast<size_t>(n))) != LS_OK) return st;
   const size_t nn = static_cast<size_t>(n);
-  LSB_CUDA(cudaMemcpyAsync(w.feats, feats, nn * 72, cudaMemcpyHostToDevice, w.stream));
-  launch_score(w.feats, n, to_dmodel(model), w.pred, w.stream);
+  if ((st = grow(w, 9 * nn, nn)) != LS_OK) return st;
+  double* d_feats = reinterpret_cast<double*>(w.d_in);
+  double* d_pred = reinterpret_cast<double*>(w.d_out);
+  LSB_CUDA(cudaMemcpyAsync(d_feats, feats, nn * 72, cudaMemcpyHostToDevice, w.stream));
+  launch_score(d_feats, n, to_dmodel(model), d_pred, w.stream);
   LSB_CUDA(cudaGetLastError());
-  LSB_CUDA(cudaMemcpyAsync(out, w.pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
+  LSB_CUDA(cudaMemcpyAsync(out, d_pred, nn * 8, cudaMemcpyDeviceToHost, w.stream));
   LSB_CUDA(cudaStreamSynchronize(w.stream));
   return LS_OK;
 }

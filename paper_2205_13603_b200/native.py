@@ -176,9 +176,23 @@ def text_array(programs):
     return arr, lens, enc
 
 
+_SPEC_CACHE: dict = {}
+
+
 def machine_spec_c(spec=None) -> MachineSpecC:
     """From a reference MachineSpec, a dict, or None (defaults of
-    `src/machine.py:22-31`)."""
+    `src/machine.py:22-31`); memoized for hashable specs (the search passes
+    the same frozen MachineSpec on every call)."""
+    try:
+        hit = _SPEC_CACHE.get(spec)
+    except TypeError:
+        return _machine_spec_c(spec)
+    if hit is None:
+        hit = _SPEC_CACHE[spec] = _machine_spec_c(spec)
+    return hit
+
+
+def _machine_spec_c(spec=None) -> MachineSpecC:
     d = {"cores": 4, "vector_lanes": 8, "cache_capacity": 4096, "hit_cost": 1,
          "miss_cost": 8, "flop_cost": 1, "unroll_discount": 0.9, "tensor_unit_cost": 8}
     if spec is not None:
