@@ -120,3 +120,32 @@ def test_lookahead_cuts_k7_launches_and_keeps_the_report(name):
         assert got["best"] == want["best"]
         launches[la] = plugin.last_tune_stats["k7_featurize_launches"]
     assert launches[True] * 10 < launches[False], launches
+
+
+def test_gpu_task_pool_waves_match_in_process_rounds():
+    # SURVEY §8 f3 on the GPU: BERT-base tasks tuned in task-parallel waves
+    # through GpuTaskPool (one worker process per device; here two workers
+    # share device 0) give exactly the allocation and objective of the same
+    # waves run in-process (parity mode: exact latencies, deterministic)
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2205_13603_b200.scorer import GpuScorer
+    from paper_2205_13603_b200.task_scheduler import GpuTaskPool, TaskScheduler, bert_tasks
+    from paper_2205_13603_b200.tensor_core import b200_space, b200_space_config
+
+    def sched():
+        return TaskScheduler(bert_tasks(scale=4), 96, round_trials=16, batch=8, population=16, seed=3,
+                             generator_for=lambda t: b200_space(), mode="parity", scorer=GpuScorer(0))
+
+    pool = GpuTaskPool([0, 0], b200_space_config(), mode="parity")
+    try:
+        a = sched().run(parallel=2, submit=pool.submit)
+    finally:
+        pool.close()
+    ex = ThreadPoolExecutor(max_workers=2)
+    try:
+        b = sched().run(parallel=2, submit=lambda s, t, cfg: ex.submit(s.execute_round, t, cfg))
+    finally:
+        ex.shutdown()
+    assert [(r["task"], r["trials"]) for r in a["allocation"]] == [(r["task"], r["trials"]) for r in b["allocation"]]
+    assert a["objective_exact"] == b["objective_exact"]
+    assert a["trials"] == b["trials"] <= 96 and a["trials"] > 40
