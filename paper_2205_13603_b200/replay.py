@@ -154,6 +154,9 @@ def lazy_program_class():
             def root(self):
                 return self._tree().root
 
+            def __reduce__(self):  # picklable (reports cross GpuTaskPool's process boundary)
+                return (_lazy_from_text, (self._ls_text, getattr(self, "_ls_hash", None)))
+
             def __eq__(self, other):  # equal to the reference object it stands for
                 if isinstance(other, ir.TensorProgram):
                     return (self.buffers, self.root) == (other.buffers, other.root)
@@ -164,6 +167,13 @@ def lazy_program_class():
 
         _LAZY = LazyProgram
     return _LAZY
+
+
+def _lazy_from_text(text: str, h=None):
+    p = lazy_program_class()(text)
+    if h is not None:
+        object.__setattr__(p, "_ls_hash", h)
+    return p
 
 
 def normalized_trace(key: str, text: str, t):
