@@ -158,3 +158,15 @@ def test_native_resample_equals_reference_resample(name):
             assert norm == ls.trace.serialize_trace(nt)
             n += 1
     assert n >= 60
+
+
+@needs_reference
+def test_lazy_program_pickles_by_text():
+    import pickle
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.replay import lazy_program_class
+    ls = loopsched()
+    text = ls.ir.serialize(ls.gmm(8, 8, 8))
+    p = lazy_program_class()(text)
+    q = pickle.loads(pickle.dumps(p))
+    assert q == p and q._ls_text == text and ls.ir.serialize(q) == text
