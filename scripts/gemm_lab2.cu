@@ -38,6 +38,7 @@ struct P {
   uint32_t* cnt;
   uint32_t* flag;
   uint32_t idesc, cols;  // cols: TMEM columns per accumulator (power of 2 >= BN)
+  uint32_t alloc;        // TMEM columns allocated: power of 2 >= cols * U
 };
 
 __global__ void __launch_bounds__(192, 1)
@@ -66,7 +67,7 @@ lab2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_slot)),
-                 "r"(p.cols * p.U)
+                 "r"(p.alloc)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -161,9 +162,11 @@ lab2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap
       if (threadIdx.x == 0) {
         const int tile = uidx[j] % tiles;
         const uint32_t t = s_ticket[j];
-        if (t % static_cast<uint32_t>(p.S) != 0)
-          while (ld_acquire_u32(p.flag + tile) < t / static_cast<uint32_t>(p.S) + 1) {
-          }
+        if (t % static_cast<uint32_t>(p.S) != 0) {
+          uint32_t spins = 0;
+          while (ld_acquire_u32(p.flag + tile) < t / static_cast<uint32_t>(p.S) + 1)
+            if (++spins > (1u << 26)) __trap();
+        }
         fence_proxy_async_global();
         for (int c0 = 0; c0 < p.BN; c0 += 32) tma_reduce_add_3d(&tc, stg + (c0 / 32) * 16384, tile * p.BN + c0, 0, 0);
         bulk_commit();
@@ -174,7 +177,7 @@ lab2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.cols * p.U) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.alloc) : "memory");
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -284,10 +287,15 @@ int main() {
     uint32_t cols = 32;
     while (cols < static_cast<uint32_t>(v.BN)) cols <<= 1;
     p.cols = cols;
-    if (cols * v.U > 512) continue;
+    p.alloc = 32;
+    while (p.alloc < cols * v.U) p.alloc <<= 1;
+    if (p.alloc > 512) continue;
     const int smem = 1024 + p.ST * (kA + v.BN * 128) + (v.BN / 32) * 16384 + 16 * p.ST + 8 * v.U + 64;
     if (smem > optin - 1024) continue;
     CUtensorMap tmb = map3(db, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, N, 64, v.BN);
+    CK(cudaStreamSynchronize(st));  // the previous variant's graph ran on st (non-blocking)
+    const int per_sm = std::min(optin / smem, 512 / static_cast<int>(p.alloc));
+    if (per_sm * 148 < (p.units + v.U - 1) / v.U) continue;  // split-K flags need co-residency
     CK(cudaMemset(dcnt, 0, 4096 * 4));
     CK(cudaMemset(dflag, 0, 4096 * 4));
     cudaLaunchConfig_t cfg = {};
@@ -305,6 +313,7 @@ int main() {
     CK(cudaMemset(dc, 0xff, M * N * 4));
     CK(cudaLaunchKernelEx(&cfg, lab2, tma, tmb, tmc, p));
     CK(cudaStreamSynchronize(st));
+    fprintf(stderr, "variant BN%d S%d U%d launched ok\n", v.BN, v.S, v.U);
     std::vector<float> hc(M * N);
     CK(cudaMemcpy(hc.data(), dc, M * N * 4, cudaMemcpyDeviceToHost));
     bool exact = true;
