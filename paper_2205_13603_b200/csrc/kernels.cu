@@ -198,10 +198,6 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, __nv_bflo
 }
 
 }  // namespace
-int opt_in_dynamic_smem(const void* fn);
-namespace {
-
-}  // namespace
 
 int opt_in_dynamic_smem(const void* fn) {
   int dev = 0, optin = 0;

@@ -90,6 +90,7 @@ constexpr int kTcSyncSlots = 4096;  // ticket slots per candidate (mode 2)
 struct TcGeom {
   int mode = 0;
   bool tma_epi = false;     // BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
+  bool direct = false;      // mode 0, BN <= 32: TMEM -> registers -> global, no staging
   int ld = 0;               // padded fp32 row of the staged tile (generic epilogue)
   int64_t stage_bytes = 0;  // one k-tile: A 128x64 + B BNx64 bf16
   int64_t ring = 0, tile = 0, smem = 0;
@@ -97,12 +98,15 @@ struct TcGeom {
 inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles) {
   TcGeom g;
   g.mode = splits == 1 ? 0 : tiles <= kTcSyncSlots ? 2 : 3;
-  g.tma_epi = bn % 32 == 0 && g.mode != 3;
+  // no split and a narrow tile: each thread stores its TMEM row straight from
+  // registers (bmm QK^T BN 16: 2.08 vs 2.40 us staged, profiles/r02_gemm_lab.md §5)
+  g.direct = g.mode == 0 && bn <= 32;
+  g.tma_epi = bn % 32 == 0 && g.mode != 3 && !g.direct;
   g.ld = static_cast<int>(bn + 4);  // padded fp32 row (16-byte aligned, conflict-free)
   g.stage_bytes = 128 * 64 * 2 + bn * 64 * 2;
   g.ring = stages * g.stage_bytes;
   // staged accumulator tile, overlays the finished ring
-  g.tile = g.tma_epi ? (bn / 32) * 16384 : 128LL * g.ld * 4;
+  g.tile = g.direct ? 0 : g.tma_epi ? (bn / 32) * 16384 : 128LL * g.ld * 4;
   g.smem = 1024 + std::max(g.ring, g.tile) + 256;
   return g;
 }

@@ -168,8 +168,8 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   }
   const KCoord* kc = a.kc + blockIdx.z * a.kt;
 
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // trigger after the wait: see tc_gemm.cu
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tile = blockIdx.y * gridDim.x + blockIdx.x;
   const int live = nbox * kRows;  // accumulator rows that hold output pixels
   // row r (0..live-1): box r / 64, pixel r % 64 of that box

@@ -44,8 +44,7 @@ struct TcArgs {
   float* c;
   int64_t sc_b, sc_m;
   int bn, splits, kt, stages;
-  int mode, ld;
-  int tma_epi;                // 32-column 128B-swizzled chunks, TMA store / add-reduce
+  int ld;
   uint32_t* sync;             // mode 2: [kTcSyncSlots] tickets, then [kTcSyncSlots] ready flags
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA)
   uint32_t idesc;
@@ -54,9 +53,19 @@ struct TcArgs {
 
 constexpr int kTile = 128 * 64 * 2;  // A stage bytes
 
+// epilogue kinds
+constexpr int kEpiStaged = 0;  // padded smem tile, thread float4 stores / red.add (BN % 32 != 0, mode 3)
+constexpr int kEpiTma = 1;     // 32-column 128B-swizzled chunks, TMA store / add-reduce
+constexpr int kEpiDirect = 2;  // mode 0, BN <= 32: each thread stores its TMEM row from registers
+
+// One instantiation per (split-K mode, epilogue, tracing): every launch runs
+// straight-line code for its own case (the all-cases kernel measured 0.5 us
+// slower per bmm launch, profiles/r02_gemm_lab.md §5).
+template <int MODE, int EPI, bool TRACE>
 __global__ void __launch_bounds__(128, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                const __grid_constant__ CUtensorMap tmc, TcArgs a) {
+  static_assert(EPI != kEpiDirect || MODE == 0, "direct epilogue stores: no split");
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
@@ -66,18 +75,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   const uint32_t a0 = base;                     // A stages
   const uint32_t b0 = base + a.stages * kTile;  // B stages
   const uint32_t ring = static_cast<uint32_t>(a.stages * (kTile + b_bytes));
-  const uint32_t tile_bytes = a.tma_epi ? static_cast<uint32_t>(a.bn / 32) * 16384u
-                                        : static_cast<uint32_t>(128 * a.ld * 4);
+  const uint32_t tile_bytes = EPI == kEpiDirect ? 0u
+                              : EPI == kEpiTma  ? static_cast<uint32_t>(a.bn / 32) * 16384u
+                                                : static_cast<uint32_t>(128 * a.ld * 4);
   const uint32_t bars = (base + (ring > tile_bytes ? ring : tile_bytes) + 15u) & ~15u;
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (done + 8 - base));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_blk = blockIdx.x, m_blk = blockIdx.y;
-  const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = gtime();
-  const int batch = blockIdx.z / a.splits, split = blockIdx.z % a.splits;
+  unsigned long long* tr = nullptr;
+  if constexpr (TRACE) {
+    const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    tr = a.trace + 8 * cta;
+    if (threadIdx.x == 0) tr[0] = gtime();
+  }
+  const int batch = MODE == 0 ? static_cast<int>(blockIdx.z) : static_cast<int>(blockIdx.z) / a.splits;
+  const int split = MODE == 0 ? 0 : static_cast<int>(blockIdx.z) % a.splits;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -99,59 +113,73 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (tr && threadIdx.x == 0) tr[1] = gtime();
+  if (TRACE && threadIdx.x == 0) tr[1] = gtime();
 
   const uint32_t stage_bytes = kTile + b_bytes;
-  // programmatic dependent launch: the next grid may start its prologue now;
-  // this grid waits for its predecessor before its first global access
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-
   const int tile = (batch * gridDim.y + m_blk) * gridDim.x + n_blk;
   float* ctile = a.c + batch * a.sc_b + static_cast<int64_t>(m_blk) * 128 * a.sc_m + static_cast<int64_t>(n_blk) * a.bn;
   const int c4 = a.bn / 4;
-  if (a.mode == 2 && warp >= 2) {
-    // every CTA takes its arrival ticket now (off the critical path); the
-    // first CTA of the tile to start zeroes it while its operands stream in
-    const int t2 = threadIdx.x - 64;
-    if (t2 == 0) s_ticket = atomicAdd(a.sync + tile, 1u);
-    asm volatile("bar.sync 1, 64;" ::: "memory");
-    const uint32_t t = s_ticket;
-    if (t % static_cast<uint32_t>(a.splits) == 0) {
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int e = t2; e < 128 * c4; e += 64) {
-        const int r = e / c4, cc = (e % c4) * 4;
-        *reinterpret_cast<float4*>(ctile + static_cast<int64_t>(r) * a.sc_m + cc) = z;
-      }
+  // programmatic dependent launch: this grid waits for its predecessor before
+  // its first global access, then lets the next grid start its prologue.
+  // Triggering only after the wait keeps at most one grid ahead resident: a
+  // trigger before the wait lets a whole chain of waiting grids pile onto the
+  // SMs (bmm 2.91 -> 1.84 us per launch in a 2000-launch chain,
+  // profiles/r02_gemm_lab.md §5)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if constexpr (MODE == 2) {
+    if (warp >= 2) {
+      // every CTA takes its arrival ticket now (off the critical path); the
+      // first CTA of the tile to start zeroes it while its operands stream in
+      const int t2 = threadIdx.x - 64;
+      if (t2 == 0) s_ticket = atomicAdd(a.sync + tile, 1u);
       asm volatile("bar.sync 1, 64;" ::: "memory");
-      if (t2 == 0) st_release_u32(a.sync + kTcSyncSlots + tile, t / static_cast<uint32_t>(a.splits) + 1);
+      const uint32_t t = s_ticket;
+      if (t % static_cast<uint32_t>(a.splits) == 0) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = t2; e < 128 * c4; e += 64) {
+          const int r = e / c4, cc = (e % c4) * 4;
+          *reinterpret_cast<float4*>(ctile + static_cast<int64_t>(r) * a.sc_m + cc) = z;
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (t2 == 0) st_release_u32(a.sync + kTcSyncSlots + tile, t / static_cast<uint32_t>(a.splits) + 1);
+      }
     }
   }
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    for (int kt = 0; kt < a.kt; ++kt) {
-      const int s = kt % a.stages;
-      const uint32_t ph = (kt / a.stages) & 1;
-      const int kc = (split * a.kt + kt) * 64;
+    int s = 0;
+    uint32_t ph = 0;
+    int kc = split * a.kt * 64;
+    for (int kt = 0; kt < a.kt; ++kt, kc += 64) {
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
       mbar_expect_tx(full + 8 * s, stage_bytes);
       tma_load_3d(a0 + s * kTile, &tma, full + 8 * s, kc, m_blk * 128, batch);
       tma_load_3d(b0 + s * b_bytes, &tmb, full + 8 * s, kc, n_blk * a.bn, batch);
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
+    int s = 0;
+    uint32_t ph = 0;
     for (int kt = 0; kt < a.kt; ++kt) {
-      const int s = kt % a.stages;
-      const uint32_t ph = (kt / a.stages) & 1;
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
-      if (tr && kt == 0) tr[2] = gtime();
+      if (TRACE && kt == 0) tr[2] = gtime();
       const uint32_t sa = a0 + s * kTile, sb = b0 + s * b_bytes;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
       if (kt + a.stages < a.kt) umma_commit(empty + 8 * s);  // the slot is refilled
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
     umma_commit(done);
   }
@@ -160,71 +188,89 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
-  if (tr && threadIdx.x == 0) tr[3] = gtime();
+  if (TRACE && threadIdx.x == 0) tr[3] = gtime();
   const int row = warp * 32 + lane;  // TMEM lane == output row of this thread
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  if (a.tma_epi) {
-    // TMEM -> 32-column chunks [128][32] fp32 with the 128-byte swizzle the C
-    // tensor map expects (16-byte unit q of row r at q ^ (r & 7): conflict-free)
-    for (int c0 = 0; c0 < a.bn; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld16_nowait(trow + c0, v);
-      tmem_ld16_nowait(trow + c0 + 16, v + 16);
-      tmem_wait();
-      uint8_t* chunk = gbase + (c0 / 32) * 16384 + row * 128;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<float4*>(chunk + ((q ^ (row & 7)) << 4)) =
-            make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
-                        __uint_as_float(v[4 * q + 3]));
-    }
-    fence_proxy_async_smem();  // read by the TMA engine
-  } else {
-    // TMEM -> padded smem tile over the finished ring (BN = 16 (mod 32))
-    float* stg = reinterpret_cast<float*>(gbase) + row * a.ld;
+  if constexpr (EPI == kEpiDirect) {
+    // TMEM -> registers -> the thread's own output row (64-128 contiguous bytes)
+    float* dst = ctile + static_cast<int64_t>(row) * a.sc_m;
     for (int c0 = 0; c0 < a.bn; c0 += 16) {
       uint32_t v[16];
       tmem_ld16_nowait(trow + c0, v);
       tmem_wait();
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float4*>(stg + c0 + 4 * q) =
+        *reinterpret_cast<float4*>(dst + c0 + 4 * q) =
             make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
                         __uint_as_float(v[4 * q + 3]));
     }
-  }
-  __syncthreads();
-  if (tr && threadIdx.x == 0) tr[4] = gtime();
-
-  if (a.mode == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
-    if (threadIdx.x == 0)
-      while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
-      }
-    __syncthreads();
-  }
-  if (tr && threadIdx.x == 0) tr[5] = gtime();
-  if (a.tma_epi) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_global();  // the (acquired) zeroing precedes the async-proxy reduction
-      for (int c0 = 0; c0 < a.bn; c0 += 32) {
-        const uint32_t src = base + (c0 / 32) * 16384;
-        if (a.mode == 0) tma_store_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
-        else tma_reduce_add_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
-      }
-      bulk_commit();
-      bulk_wait_all();
-    }
+    if (TRACE && threadIdx.x == 0) tr[4] = tr[5] = gtime();
   } else {
-    const float* stile = reinterpret_cast<const float*>(gbase);
-    for (int e = threadIdx.x; e < 128 * c4; e += 128) {
-      const int r = e / c4, cc = (e % c4) * 4;
-      const float4 acc = *reinterpret_cast<const float4*>(stile + r * a.ld + cc);
-      float* dst = ctile + static_cast<int64_t>(r) * a.sc_m + cc;
-      if (a.mode == 0) *reinterpret_cast<float4*>(dst) = acc;
-      else red_add_f4(dst, acc);
+    if constexpr (EPI == kEpiTma) {
+      // TMEM -> 32-column chunks [128][32] fp32 with the 128-byte swizzle the C
+      // tensor map expects (16-byte unit q of row r at q ^ (r & 7): conflict-free)
+      for (int c0 = 0; c0 < a.bn; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld16_nowait(trow + c0, v);
+        tmem_ld16_nowait(trow + c0 + 16, v + 16);
+        tmem_wait();
+        uint8_t* chunk = gbase + (c0 / 32) * 16384 + row * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(chunk + ((q ^ (row & 7)) << 4)) =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                          __uint_as_float(v[4 * q + 3]));
+      }
+      fence_proxy_async_smem();  // read by the TMA engine
+    } else {
+      // TMEM -> padded smem tile over the finished ring (BN = 16 (mod 32))
+      float* stg = reinterpret_cast<float*>(gbase) + row * a.ld;
+      for (int c0 = 0; c0 < a.bn; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16_nowait(trow + c0, v);
+        tmem_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stg + c0 + 4 * q) =
+              make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                          __uint_as_float(v[4 * q + 3]));
+      }
+    }
+    __syncthreads();
+    if (TRACE && threadIdx.x == 0) tr[4] = gtime();
+
+    if constexpr (MODE == 2) {
+      if (s_ticket % static_cast<uint32_t>(a.splits) != 0) {
+        if (threadIdx.x == 0)
+          while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
+          }
+        __syncthreads();
+      }
+    }
+    if (TRACE && threadIdx.x == 0) tr[5] = gtime();
+    if constexpr (EPI == kEpiTma) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async_global();  // the (acquired) zeroing precedes the async-proxy reduction
+        for (int c0 = 0; c0 < a.bn; c0 += 32) {
+          const uint32_t src = base + (c0 / 32) * 16384;
+          if constexpr (MODE == 0) tma_store_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
+          else tma_reduce_add_3d(&tmc, src, n_blk * a.bn + c0, m_blk * 128, batch);
+        }
+        bulk_commit();
+        bulk_wait_all();
+      }
+    } else {
+      const float* stile = reinterpret_cast<const float*>(gbase);
+      for (int e = threadIdx.x; e < 128 * c4; e += 128) {
+        const int r = e / c4, cc = (e % c4) * 4;
+        const float4 acc = *reinterpret_cast<const float4*>(stile + r * a.ld + cc);
+        float* dst = ctile + static_cast<int64_t>(r) * a.sc_m + cc;
+        if constexpr (MODE == 0) *reinterpret_cast<float4*>(dst) = acc;
+        else red_add_f4(dst, acc);
+      }
     }
   }
-  if (tr && threadIdx.x == 0) {
+  if (TRACE && threadIdx.x == 0) {
     tr[6] = gtime();
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -237,13 +283,49 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   }
 }
 
+using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcArgs);
+
+// the instantiations: (mode, epilogue) pairs tc_geom can produce, x tracing
+template <bool TRACE>
+TcKernel pick_kernel(int mode, int epi) {
+  if (mode == 0) {
+    if (epi == kEpiDirect) return tc_gemm_kernel<0, kEpiDirect, TRACE>;
+    if (epi == kEpiTma) return tc_gemm_kernel<0, kEpiTma, TRACE>;
+    return tc_gemm_kernel<0, kEpiStaged, TRACE>;
+  }
+  if (mode == 2) return epi == kEpiTma ? tc_gemm_kernel<2, kEpiTma, TRACE> : tc_gemm_kernel<2, kEpiStaged, TRACE>;
+  return tc_gemm_kernel<3, kEpiStaged, TRACE>;
+}
+
+TcKernel kernel_for(const TcGeom& g, bool trace) {
+  const int epi = g.direct ? kEpiDirect : g.tma_epi ? kEpiTma : kEpiStaged;
+  return trace ? pick_kernel<true>(g.mode, epi) : pick_kernel<false>(g.mode, epi);
+}
+
+// the smem opt-in of every instantiation (identical static smem), once
+int tc_max_dyn() {
+  static int max_dyn = [] {
+    int m = 1 << 30;
+    for (int mode : {0, 2, 3})
+      for (int epi : {kEpiStaged, kEpiTma, kEpiDirect})
+        for (bool t : {false, true}) {
+          if (epi == kEpiDirect && mode != 0) continue;
+          if (mode == 3 && epi != kEpiStaged) continue;
+          const int d = opt_in_dynamic_smem(reinterpret_cast<const void*>(t ? pick_kernel<true>(mode, epi)
+                                                                             : pick_kernel<false>(mode, epi)));
+          m = std::min(m, d);
+        }
+    return m;
+  }();
+  return max_dyn;
+}
+
 }  // namespace
 
-void preload_tc_gemm() { opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_gemm_kernel)); }
+void preload_tc_gemm() { tc_max_dyn(); }
 
 bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
-  static int max_dyn = -1;
-  if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_gemm_kernel));
+  const int max_dyn = tc_max_dyn();
   if (max_dyn <= 0 || L.smem_bytes > max_dyn) return false;
   const TcGeom g = tc_geom(L.bn, L.splits, L.stages, static_cast<int64_t>(L.batch) * L.grid_m * L.grid_n);
   if (g.mode == 2 && !L.sync) return false;
@@ -256,9 +338,7 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.splits = L.splits;
   a.kt = L.kt;
   a.stages = L.stages;
-  a.mode = g.mode;
   a.ld = g.ld;
-  a.tma_epi = g.tma_epi ? 1 : 0;
   a.sync = L.sync;
   a.trace = L.trace;
   // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N>>3, M>>4
@@ -281,7 +361,7 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   const CUtensorMap ta = *static_cast<const CUtensorMap*>(L.tmap_a);
   const CUtensorMap tb = *static_cast<const CUtensorMap*>(L.tmap_b);
   const CUtensorMap tc = L.tmap_c ? *static_cast<const CUtensorMap*>(L.tmap_c) : tb;
-  if (cudaLaunchKernelEx(&cfg, tc_gemm_kernel, ta, tb, tc, a) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&cfg, kernel_for(g, L.trace != nullptr), ta, tb, tc, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
