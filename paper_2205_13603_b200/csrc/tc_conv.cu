@@ -99,9 +99,12 @@ void host_add_parts(const CList& L, int64_t idx, Coord& a) {
   }
 }
 
+// one instantiation per (split-K mode, epilogue, tracing), as tc_gemm.cu
+template <int MODE, bool TMA_EPI, bool TRACE>
 __global__ void __launch_bounds__(128, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                const __grid_constant__ CUtensorMap tmc, const __grid_constant__ TcConvArgs a) {
+  static_assert(!(TMA_EPI && MODE == 1), "the cluster reduction stores from registers");
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
@@ -112,19 +115,22 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   const uint32_t b0 = base + a.stages * kStageA;
   const int red_ld = a.bn + 4;
   const uint32_t stage_end = b0 + a.stages * b_bytes;
-  const int S_cl = a.mode == 1 ? a.splits : 1;
+  const int S_cl = MODE == 1 ? a.splits : 1;
   const int rows_per = (kRows + S_cl - 1) / S_cl;
-  const uint32_t red = a.mode == 1 ? ((stage_end + 15u) & ~15u) : base;
-  const uint32_t red_bytes = a.mode == 1 ? static_cast<uint32_t>(S_cl * rows_per * red_ld * 4)
-                                         : static_cast<uint32_t>((a.pair ? 2 : 1) * kRows * red_ld * 4);
+  const uint32_t red = MODE == 1 ? ((stage_end + 15u) & ~15u) : base;
+  const uint32_t red_bytes = MODE == 1 ? static_cast<uint32_t>(S_cl * rows_per * red_ld * 4)
+                                       : static_cast<uint32_t>((a.pair ? 2 : 1) * kRows * red_ld * 4);
   const uint32_t red_end = red + red_bytes;
   const uint32_t bars = ((stage_end > red_end ? stage_end : red_end) + 15u) & ~15u;
   const uint32_t full = bars, empty = bars + 8 * a.stages, done = bars + 16 * a.stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bars - base) + 16 * a.stages + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  unsigned long long* tr = a.trace ? a.trace + 8 * cta : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = gtime();
+  unsigned long long* tr = nullptr;
+  if constexpr (TRACE) {
+    const size_t cta = (static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    tr = a.trace + 8 * cta;
+    if (threadIdx.x == 0) tr[0] = gtime();
+  }
 
   // The dead lower half of every A stage (rows 64..127) is left as it is:
   // row r of the accumulator depends on A row r only, and rows 64..127 are
@@ -151,7 +157,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (tr && threadIdx.x == 0) tr[1] = gtime();
+  if (TRACE && threadIdx.x == 0) tr[1] = gtime();
 
   // tile origin: output-pixel box (grid y; a pair of boxes with `pair`),
   // channel tile (grid x), split (grid z)
@@ -179,7 +185,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     return cb + (r >> 3) * a.cc_h1 + (r & 7) * a.cc_w1;
   };
   const int c4 = a.bn / 4;
-  if (a.mode == 2 && warp >= 2) {
+  if (MODE == 2 && warp >= 2) {
     // split-K through L2 (as tc_gemm.cu mode 2): arrival ticket per tile; the
     // first CTA of the tile to start zeroes its 64 x BN output box while its
     // operands stream in and releases this launch's epoch
@@ -201,9 +207,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
     const uint32_t stage_bytes = nbox * kLiveA + b_bytes;
+    int s = 0;
+    uint32_t ph = 0;
     for (int kt = 0; kt < a.kt; ++kt) {
-      const int s = kt % a.stages;
-      const uint32_t ph = (kt / a.stages) & 1;
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
       const KCoord k = kc[kt];
       mbar_expect_tx(full + 8 * s, stage_bytes);
@@ -213,20 +219,28 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         tma_load_4d(a0 + s * kStageA + kLiveA, &tmx, full + 8 * s, static_cast<int>(o1.c) + k.c,
                     static_cast<int>(o1.w) + k.w, static_cast<int>(o1.h) + k.h, static_cast<int>(o1.n) + k.n);
       tma_load_3d(b0 + s * b_bytes, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf, static_cast<int>(o.co), 0);
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer (single thread) ----
+    int s = 0;
+    uint32_t ph = 0;
     for (int kt = 0; kt < a.kt; ++kt) {
-      const int s = kt % a.stages;
-      const uint32_t ph = (kt / a.stages) & 1;
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
-      if (tr && kt == 0) tr[2] = gtime();
+      if (TRACE && kt == 0) tr[2] = gtime();
       const uint32_t sa = a0 + s * kStageA, sb = b0 + s * b_bytes;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
       umma_commit(empty + 8 * s);
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1;
+      }
     }
     umma_commit(done);
   }
@@ -235,9 +249,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
-  if (tr && threadIdx.x == 0) tr[3] = gtime();
+  if (TRACE && threadIdx.x == 0) tr[3] = gtime();
   const int row = warp * 32 + lane;
-  if (a.mode == 1) {
+  if constexpr (MODE == 1) {
     const uint32_t me = cluster_rank();
     if (warp < 2) {
       const int owner = row / rows_per, lr = row - owner * rows_per;
@@ -267,7 +281,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         }
       *reinterpret_cast<float4*>(out_row(r_lo + lr2) + cc) = acc;
     }
-  } else if (a.tma_epi) {
+  } else if constexpr (TMA_EPI) {
     // TMEM rows -> per box [64 px][32 ch] fp32 chunks, 128-byte swizzle (unit
     // q of row r at q ^ (r & 7)), then one 4-D TMA store / add-reduce per chunk
     const int nch = a.bn / 32;
@@ -288,14 +302,14 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (tr && threadIdx.x == 0) tr[4] = gtime();
-    if (a.mode == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
+    if (TRACE && threadIdx.x == 0) tr[4] = gtime();
+    if (MODE == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
       if (threadIdx.x == 0)
         while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
         }
       __syncthreads();
     }
-    if (tr && threadIdx.x == 0) tr[5] = gtime();
+    if (TRACE && threadIdx.x == 0) tr[5] = gtime();
     if (threadIdx.x == 0) {
       fence_proxy_async_global();
       for (int b = 0; b < nbox; ++b) {
@@ -308,7 +322,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
         const int n0 = static_cast<int>(off / a.oshape[1]);
         for (int c0 = 0; c0 < a.bn; c0 += 32) {
           const uint32_t src = base + (b * nch + c0 / 32) * 8192;
-          if (a.mode == 2) tma_reduce_add_4d(&tmc, src, co0 + c0, q0, p0, n0);
+          if constexpr (MODE == 2) tma_reduce_add_4d(&tmc, src, co0 + c0, q0, p0, n0);
           else tma_store_4d(&tmc, src, co0 + c0, q0, p0, n0);
         }
       }
@@ -328,23 +342,23 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
       }
     }
     __syncthreads();
-    if (tr && threadIdx.x == 0) tr[4] = gtime();
-    if (a.mode == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
+    if (TRACE && threadIdx.x == 0) tr[4] = gtime();
+    if (MODE == 2 && s_ticket % static_cast<uint32_t>(a.splits) != 0) {
       if (threadIdx.x == 0)
         while (ld_acquire_u32(a.sync + kTcSyncSlots + tile) < s_ticket / static_cast<uint32_t>(a.splits) + 1) {
         }
       __syncthreads();
     }
-    if (tr && threadIdx.x == 0) tr[5] = gtime();
+    if (TRACE && threadIdx.x == 0) tr[5] = gtime();
     const float* sb = reinterpret_cast<const float*>(gbase);
     for (int e = threadIdx.x; e < live * c4; e += 128) {
       const int r = e / c4, cc = (e % c4) * 4;
       const float4 v = *reinterpret_cast<const float4*>(sb + r * red_ld + cc);
-      if (a.mode == 2) red_add_f4(out_row(r) + cc, v);
+      if constexpr (MODE == 2) red_add_f4(out_row(r) + cc, v);
       else *reinterpret_cast<float4*>(out_row(r) + cc) = v;
     }
   }
-  if (tr && threadIdx.x == 0) {
+  if (TRACE && threadIdx.x == 0) {
     tr[6] = gtime();
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -357,15 +371,44 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   }
 }
 
+using ConvKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcConvArgs);
+
+template <bool TRACE>
+ConvKernel pick_conv(int mode, bool tma_epi) {
+  if (mode == 1) return tc_conv_kernel<1, false, TRACE>;
+  if (mode == 2) return tma_epi ? tc_conv_kernel<2, true, TRACE> : tc_conv_kernel<2, false, TRACE>;
+  return tma_epi ? tc_conv_kernel<0, true, TRACE> : tc_conv_kernel<0, false, TRACE>;
+}
+
+// smem opt-in (and the non-portable cluster size of the mode-1 kernels) of
+// every instantiation, once
+int conv_max_dyn() {
+  static int max_dyn = [] {
+    int m = 1 << 30;
+    for (int mode : {0, 1, 2})
+      for (bool epi : {false, true})
+        for (bool t : {false, true}) {
+          if (mode == 1 && epi) continue;
+          const void* fn = reinterpret_cast<const void*>(t ? pick_conv<true>(mode, epi) : pick_conv<false>(mode, epi));
+          m = std::min(m, opt_in_dynamic_smem(fn));
+          if (mode == 1 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            m = -1;
+          }
+        }
+    return m;
+  }();
+  return max_dyn;
+}
+
 }  // namespace
 
-void preload_tc_conv() { opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel)); }
+void preload_tc_conv() { conv_max_dyn(); }
 
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
                     cudaStream_t st, unsigned long long* trace, uint32_t* sync, const void* tmap_c,
                     const int64_t* oshape) {
-  static int max_dyn = -1;
-  if (max_dyn < 0) max_dyn = opt_in_dynamic_smem(reinterpret_cast<const void*>(tc_conv_kernel));
+  const int max_dyn = conv_max_dyn();
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
   if (g.splits > kMaxClusterSplits || g.grid_m > 65535 || g.grid_n > 65535) return false;
   if (g.splits * g.kt > kConvMaxK) return false;
@@ -425,14 +468,6 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && (g.bn <= 16 || ctas > 2 * 148) ? 1 : 0;
   }
   const int64_t grid_y = a.pair ? (g.grid_m + 1) / 2 : g.grid_m;
-  static bool nonportable = false;
-  if (a.mode == 1 && g.splits > 8 && !nonportable) {
-    if (cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    nonportable = true;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(g.grid_n), static_cast<unsigned>(grid_y), static_cast<unsigned>(g.splits));
   cfg.blockDim = dim3(128, 1, 1);
@@ -450,7 +485,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
   const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
   const CUtensorMap tcm = a.tma_epi ? *static_cast<const CUtensorMap*>(tmap_c) : tw;
-  if (cudaLaunchKernelEx(&cfg, tc_conv_kernel, tx, tw, tcm, a) != cudaSuccess) {
+  const ConvKernel kern = trace ? pick_conv<true>(a.mode, a.tma_epi != 0) : pick_conv<false>(a.mode, a.tma_epi != 0);
+  if (cudaLaunchKernelEx(&cfg, kern, tx, tw, tcm, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
