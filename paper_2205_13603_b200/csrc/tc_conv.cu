@@ -137,6 +137,12 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   // never read back, so whatever the smem holds there cannot reach C
   // (zeroing it cost ~0.5 us of every CTA's setup).
 
+  // this split's k-tile coordinate table, param space -> smem before the
+  // dependency wait (dynamically indexed param reads miss the constant cache
+  // on the producer's critical path)
+  __shared__ KCoord s_kc[kConvMaxK];
+  for (int i = static_cast<int>(threadIdx.x) - 64; i >= 0 && i < a.kt; i += 64) s_kc[i] = a.kc[blockIdx.z * a.kt + i];
+
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(a.tmem_cols)
@@ -172,7 +178,7 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     add_parts(a.m_grid, box0 + 1, o1);
     add_parts(a.n_grid, blockIdx.x, o1);
   }
-  const KCoord* kc = a.kc + blockIdx.z * a.kt;
+  const KCoord* kc = s_kc;
 
   asm volatile("griddepcontrol.wait;" ::: "memory");  // trigger after the wait: see tc_gemm.cu
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

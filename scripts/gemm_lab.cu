@@ -90,7 +90,6 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
   tc_fence_after();
   const uint32_t tmem = (p.skip & 4) ? 0u : *tslot;
   if (p.CN > 1) cluster_arrive();
-  if (!(p.skip & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tr && threadIdx.x == 0) tr[1] = gtime();
   // skip 64: weight (B) k-tiles of the first ring fill issued before the
   // dependency wait (read-only operand); skip 128: the A k-tiles too
@@ -104,6 +103,9 @@ lab_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUten
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // default: trigger the next grid after the wait (as the product kernel;
+  // skip 8 triggers at kernel start instead)
+  if (!(p.skip & 8)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tr && threadIdx.x == 0) tr[2] = gtime();
   if (p.CN > 1) cluster_wait();
 
