@@ -170,7 +170,8 @@ ls_status ls_runner_launch_count(ls_runner* r, int64_t* count);
  * phase-B enqueue ms, [2] device spin us.  Passing n > 7 with out[7] > 0 sets
  * the per-call host cost (us) used to size the spin. */
 ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n);
-/* Diagnostics: launch one tcgen05 candidate `launches` times back to back with
+/* Diagnostics: launch one tcgen05 candidate `launches` times back to back
+ * (one CUDA graph, PDL-chained like the timed repeats) with
  * per-CTA %globaltimer stamps (8 u64 per CTA: start, setup done, first stage
  * landed, accumulator done, partial tile staged, zeroing flag acquired,
  * stored, smid). */

@@ -1386,13 +1386,23 @@ ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int 
     cudaFree(d);
     return ps;
   }
-  bool ok = true;
+  // the launches are captured into one CUDA graph and replayed back to back,
+  // as the runner's timed repeats (PDL-chained, no host gaps)
+  bool ok = cudaStreamBeginCapture(r->cap_st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
   for (int i = 0; i < launches && ok; ++i) {
     r->trace = d + static_cast<size_t>(i) * ctas * 8;
-    ok = r->launch(plan, false, 0);
+    ok = r->launch(plan, false, 0, r->cap_st);
   }
   r->trace = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(r->cap_st, &g);
+  ok = ok && ce == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+  if (g) cudaGraphDestroy(g);
+  if (ok) ok = cudaGraphUpload(ge, r->st) == cudaSuccess && cudaGraphLaunch(ge, r->st) == cudaSuccess;
   cudaError_t e = cudaStreamSynchronize(r->st);
+  if (ge) cudaGraphExecDestroy(ge);
+  if (!ok) cudaGetLastError();
   int keep = std::min(max_ctas, ctas * launches);
   if (ok && e == cudaSuccess)
     e = cudaMemcpy(out, d, static_cast<size_t>(keep) * 8 * 8, cudaMemcpyDeviceToHost);

@@ -1,4 +1,6 @@
-"""Per-CTA timeline of a tcgen05 candidate (globaltimer stamps)."""
+"""Per-CTA timeline of a tcgen05 candidate (globaltimer stamps), launches
+chained in one CUDA graph as the runner's timed repeats:
+  python scripts/tc_trace.py 49,1,64,3,3,3 16 conv2d"""
 import ctypes
 import os
 import sys
@@ -24,9 +26,10 @@ plans = r.plan_programs(progs)
 i = next(i for i, p in enumerate(plans) if p["family"] == family and p["cfg"][:len(want)] == want)
 print("cfg", plans[i]["cfg"][:8])
 b = progs[i].encode()
-buf = (ctypes.c_uint64 * (8 * 4096))()
+cap = 1 << 15
+buf = (ctypes.c_uint64 * (8 * cap))()
 n = ctypes.c_int()
-native.check(native.lib().ls_runner_trace_tc(r._h, b, len(b), launches, buf, 4096 // 1, ctypes.byref(n)), "trace")
+native.check(native.lib().ls_runner_trace_tc(r._h, b, len(b), launches, buf, cap, ctypes.byref(n)), "trace")
 a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8)[: n.value * launches].astype(np.int64)
 t0 = a[:, 0].min()
 for L in range(launches):
@@ -38,3 +41,9 @@ for L in range(launches):
           f"firstload+{med(2,1):.2f} mma_done+{med(3,2):.2f} staged+{med(4,3):.2f} "
           f"received+{recv:.2f} stored+{med(6,5) if recv == recv else med(6,4):.2f} "
           f"end [{rel[:,6].min():.2f},{rel[:,6].max():.2f}] us")
+ends = [a[L * n.value:(L + 1) * n.value, 6].max() for L in range(launches)]
+firsts = [a[L * n.value:(L + 1) * n.value, 2].min() for L in range(launches)]
+per = np.diff(ends) / 1000.0
+gap = (np.array(firsts[1:]) - np.array(ends[:-1])) / 1000.0
+print(f"median over launches 1..: last end -> next last end {np.median(per[1:]):.2f} us, "
+      f"last end -> next first operands landed {np.median(gap[1:]):.2f} us")
