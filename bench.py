@@ -327,7 +327,7 @@ def run_b200(args):
     # best schedule of this rank (rank 0 reports its own; all ranks see the same kinds).
     # Like a tuner's final measurement of its best records, the fastest few
     # distinct schedules of the step are re-measured with long graph repeats
-    # (>= 0.5 ms per candidate), so the per-launch time carries no graph-launch
+    # (>= 2 ms per candidate), so the per-launch time carries no graph-launch
     # overhead amortised over only 3 repeats; outside the timed region.
     ok = [r for r in results[-1] if r["status"] == "OK"]
     best = min(ok, key=lambda r: r["latency_ns"]) if ok else None
@@ -346,7 +346,9 @@ def run_b200(args):
             top.append(i)
             if len(top) == args.final_top:
                 break
-        fin = B200Runner(device=local, dtype=dtype, min_repeats=50, max_repeats=2000, target_ms=0.5,
+        # >= 200 chained launches: the per-launch time settles by then
+        # (profiles/r02_repeat_sweep.txt: 50 -> 200 repeats is 2-4 % faster, 200 -> 2000 < 1 %)
+        fin = B200Runner(device=local, dtype=dtype, min_repeats=200, max_repeats=4000, target_ms=2.0,
                          timeout_ms=timeout_ms)
         fin.set_workload(e0, inputs)
         rem = fin.measure_programs([texts[i] for i in top])
@@ -447,7 +449,7 @@ def run_b200(args):
                 "family": best["family"], "cfg": best["cfg"],
                 "repeats": best["repeats"], "latency_us_in_step": best_in_step_us,
                 "measurement": f"top {args.final_top} distinct schedules of the last step re-measured, "
-                               "CUDA graph of >= 50 back-to-back launches (>= 0.5 ms) between CUDA events",
+                               "CUDA graph of >= 200 back-to-back launches (>= 2 ms) between CUDA events",
                 "speedup_vs_e0": base["latency_ns"] / best["latency_ns"]},
             "e0_baseline_us": base["latency_ns"] / 1e3,
             "parity_mode": {
