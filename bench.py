@@ -401,6 +401,17 @@ def run_b200(args):
         iso.close()
         isolated_us = statistics.median(vals) if vals else None
 
+    # cold-L2 latency of the best schedule (SURVEY §8(d) timing protocol):
+    # every one of 20 repeats after a 256 MB scrub, timed alone
+    cold_us = None
+    if best is not None:
+        cold = B200Runner(device=local, dtype=dtype, min_repeats=20, max_repeats=20, target_ms=0.0,
+                          timeout_ms=timeout_ms, flush_l2=True)
+        cold.set_workload(e0, inputs)
+        x, = cold.measure_programs([best_text])
+        cold.close()
+        cold_us = x["latency_ns"] / 1e3 if x["status"] == "OK" else None
+
     # parity mode end to end: the reference Runner's computation for the same
     # slice through the public API from host program texts (ls_analyze_batch)
     par_e2e = None
@@ -446,6 +457,7 @@ def run_b200(args):
                 "tflops": best_tflops, "frac_of_peak": best_tflops / peak,
                 "peak": peak, "peak_source": peak_src if dtype == "bf16" else "fp32 SIMT nominal",
                 "latency_us": best["latency_ns"] / 1e3, "isolated_us": isolated_us,
+                "cold_l2_us": cold_us,
                 "family": best["family"], "cfg": best["cfg"],
                 "repeats": best["repeats"], "latency_us_in_step": best_in_step_us,
                 "measurement": f"top {args.final_top} distinct schedules of the last step re-measured, "
@@ -467,6 +479,7 @@ def run_b200(args):
                 "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
                 "traffic": traffic_bytes, "traffic_source": traffic_src,
                 "frac_isolated": None if not isolated_us else flops / (isolated_us * 1e-6) / 1e12 / peak,
+                "frac_cold_l2": None if not cold_us else flops / (cold_us * 1e-6) / 1e12 / peak,
                 "kernel": f"best candidate ({best['family']}), L2-warm back-to-back repeats"},
             "cpu_baseline": cpu,
             "reference_search": search,

@@ -97,7 +97,8 @@ typedef struct {
   double target_ms;        /* repeats sized so one candidate runs ~target_ms       */
   double timeout_ms;       /* device-side deadline cap for the checked launch      */
   double rtol, atol;       /* parity tolerance against the e0 reference output     */
-  int32_t flush_l2;        /* reserved (must be 0)                                 */
+  int32_t flush_l2;        /* nonzero: cold-L2 timing -- every timed repeat runs   */
+                           /* after a 256 MB scrub and is timed alone (no graphs) */
   int32_t carry_best;      /* nonzero: the device best-so-far behind timeout_factor */
                            /* deadlines persists across ls_runner_measure calls of */
                            /* one workload (small tuning batches); reset by        */

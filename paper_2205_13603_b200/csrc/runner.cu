@@ -159,6 +159,8 @@ struct ls_runner {
   std::map<int, CUtensorMap> tmap_am;  // A maps by box rows (TMA multicast slices)
   std::map<int, CUtensorMap> tmap_b;
   unsigned long long* deadline = nullptr;  // device deadline state: [0] deadline, [1] arm time, [2] best ns
+  void* scrub = nullptr;  // flush_l2: 256 MB written before every timed repeat (L2 is 126 MB)
+  static constexpr size_t kScrubBytes = 256ull << 20;
   int* flags = nullptr;                    // per-candidate timeout flags
   unsigned long long* parity = nullptr;    // per-candidate (max err bits, mismatches)
   int cap = 0;
@@ -230,6 +232,8 @@ struct ls_runner {
     if (st) cudaStreamSynchronize(st);
     release_workload();
     cudaFree(deadline); cudaFree(flags); cudaFree(parity); cudaFree(gcode); cudaFree(tcsync);
+    cudaFree(scrub);
+    scrub = nullptr;
     pool_release();
     gcode = nullptr;
     tcsync = nullptr;
@@ -1201,6 +1205,20 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       }
   }
   std::vector<cudaGraphExec_t> execs;
+  struct ColdEv {
+    int i;
+    cudaEvent_t a, b;
+  };
+  std::vector<ColdEv> cold_ev;  // flush_l2: one event pair per timed repeat
+  struct ColdEvFree {
+    std::vector<ColdEv>& v;
+    ~ColdEvFree() {
+      for (const ColdEv& c : v) {
+        cudaEventDestroy(c.a);
+        cudaEventDestroy(c.b);
+      }
+    }
+  } cold_free{cold_ev};
   const int chunk = 32;
   double prev_gpu_us = 0.0;
   for (int c0 = 0; c0 < n; c0 += chunk) {
@@ -1251,6 +1269,27 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
       // the graph's device-side upload (otherwise done by its first launch,
       // inside the timed region) precedes the start event
       if (g) LSB_CUDA(cudaGraphUpload(g, r->st));
+      if (r->opts.flush_l2) {
+        // cold-L2 latency: every repeat runs after a 256 MB scrub and is
+        // timed alone (events around the candidate's launch only)
+        if (!r->scrub) LSB_CUDA(cudaMalloc(&r->scrub, ls_runner::kScrubBytes));
+        const int rep = reps[static_cast<size_t>(i)];
+        for (int k = 0; k < rep; ++k) {
+          cudaEvent_t a, b;
+          LSB_CUDA(cudaEventCreate(&a));
+          LSB_CUDA(cudaEventCreate(&b));
+          cold_ev.push_back({i, a, b});
+          LSB_CUDA(cudaMemsetAsync(r->scrub, k & 0xff, ls_runner::kScrubBytes, r->st));
+          LSB_CUDA(cudaEventRecord(a, r->st));
+          if (!r->launch(p, false, i)) {
+            set_error("runner phase B: launch failed");
+            cudaEventDestroy(batch0);
+            return LS_ERR_CUDA;
+          }
+          LSB_CUDA(cudaEventRecord(b, r->st));
+        }
+        continue;
+      }
       LSB_CUDA(cudaEventRecord(E[4 * i + 2], r->st));
       if (g) {
         LSB_CUDA(cudaGraphLaunch(g, r->st));
@@ -1278,10 +1317,16 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
     set_error(std::string("runner phase B: ") + cudaGetErrorString(se));
     return LS_ERR_CUDA;
   }
+  std::vector<double> cold_ms(static_cast<size_t>(n), 0.0);
+  for (const ColdEv& c : cold_ev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.a, c.b) == cudaSuccess) cold_ms[static_cast<size_t>(c.i)] += ms;
+  }
   for (int i = 0; i < n; ++i) {
     if (!launched[static_cast<size_t>(i)]) continue;
     float ms = 0.f;
-    LSB_CUDA(cudaEventElapsedTime(&ms, E[4 * i + 2], E[4 * i + 3]));
+    if (r->opts.flush_l2) ms = static_cast<float>(cold_ms[static_cast<size_t>(i)]);
+    else LSB_CUDA(cudaEventElapsedTime(&ms, E[4 * i + 2], E[4 * i + 3]));
     out[i].repeats = reps[static_cast<size_t>(i)];
     out[i].latency_ns = 1e6 * static_cast<double>(ms) / reps[static_cast<size_t>(i)];
   }

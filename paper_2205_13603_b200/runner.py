@@ -45,7 +45,7 @@ class B200Runner:
                  max_repeats: int = 200, target_ms: float = 0.2, timeout_ms: float = 2.0,
                  rtol: float = 0.0, atol: float = 0.0, sentinel_factor: float = 1e4,
                  timeout_factor: float = 0.0, timeout_floor_ms: float = 0.05,
-                 single_shot_factor: float = 0.0, carry_best: bool = False):
+                 single_shot_factor: float = 0.0, carry_best: bool = False, flush_l2: bool = False):
         L = native.lib()
         o = native.RunnerOptsC()
         o.dtype = 1 if dtype == "bf16" else 0
@@ -55,6 +55,7 @@ class B200Runner:
         o.timeout_factor, o.timeout_floor_ms = timeout_factor, timeout_floor_ms
         o.single_shot_factor = single_shot_factor
         o.carry_best = 1 if carry_best else 0
+        o.flush_l2 = 1 if flush_l2 else 0  # cold-L2 timing of every repeat
         h = ctypes.c_void_p()
         native.check(L.ls_runner_create(device, ctypes.byref(o), ctypes.byref(h)),
                      "ls_runner_create")

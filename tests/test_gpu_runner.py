@@ -404,3 +404,29 @@ def test_traced_pipeline_depth_candidates_exact():
         assert res["status"] == "OK" and res["mismatches"] == 0, res
         assert np.array_equal(r.last_output().astype(np.float64), want), res["cfg"]
     r.close()
+
+
+@pytest.mark.parametrize("name", ["bert_ffn", "bmm_qk"])
+def test_cold_l2_timing_mode(name):
+    # flush_l2: every timed repeat after a 256 MB scrub, timed alone; the
+    # output after the repeats is still exact and a cold launch is no faster
+    # than the same schedule's L2-warm chained launches
+    hdr, pop = load_population(name)
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    warm = make_runner("bf16", min_repeats=50, max_repeats=50)
+    warm.set_workload(e0, seed=3)
+    plans = warm.plan_programs(progs)
+    idx = pick(plans, "tcgen05", 3)
+    assert idx
+    w = warm.measure_programs([progs[i] for i in idx])
+    warm.close()
+    cold = make_runner("bf16", min_repeats=5, max_repeats=5, flush_l2=True)
+    cold.set_workload(e0, seed=3)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 3)).values()))
+    for i, wx in zip(idx, w):
+        cx, = cold.measure_programs([progs[i]])
+        assert cx["status"] == "OK" and cx["mismatches"] == 0 and cx["repeats"] == 5, cx
+        assert np.array_equal(cold.last_output().astype(np.float64), want)
+        assert cx["latency_ns"] > 0.9 * wx["latency_ns"], (plans[i]["cfg"], cx["latency_ns"], wx["latency_ns"])
+    cold.close()
