@@ -1444,8 +1444,15 @@ ls_status ls_runner_trace_tc(ls_runner* r, const char* program, size_t len, int 
   const cudaError_t ce = cudaStreamEndCapture(r->cap_st, &g);
   ok = ok && ce == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
   if (g) cudaGraphDestroy(g);
-  if (ok) ok = cudaGraphUpload(ge, r->st) == cudaSuccess && cudaGraphLaunch(ge, r->st) == cudaSuccess;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  if (ok) ok = cudaGraphUpload(ge, r->st) == cudaSuccess && cudaEventRecord(t0, r->st) == cudaSuccess &&
+               cudaGraphLaunch(ge, r->st) == cudaSuccess && cudaEventRecord(t1, r->st) == cudaSuccess;
   cudaError_t e = cudaStreamSynchronize(r->st);
+  if (ok && e == cudaSuccess) cudaEventElapsedTime(&r->last_ms, t0, t1);  // ls_runner_elapsed_ms: the traced graph
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
   if (ge) cudaGraphExecDestroy(ge);
   if (!ok) cudaGetLastError();
   int keep = std::min(max_ctas, ctas * launches);

@@ -45,5 +45,6 @@ ends = [a[L * n.value:(L + 1) * n.value, 6].max() for L in range(launches)]
 firsts = [a[L * n.value:(L + 1) * n.value, 2].min() for L in range(launches)]
 per = np.diff(ends) / 1000.0
 gap = (np.array(firsts[1:]) - np.array(ends[:-1])) / 1000.0
+print(f"traced graph: {r.elapsed_ms() * 1e3 / launches:.2f} us per launch (CUDA events around the graph)")
 print(f"median over launches 1..: last end -> next last end {np.median(per[1:]):.2f} us, "
       f"last end -> next first operands landed {np.median(gap[1:]):.2f} us")
