@@ -74,11 +74,12 @@ def test_all_tcgen05_candidates_exact_bert_ffn():
     r.close()
 
 
-@pytest.mark.parametrize("name", ["bert_ffn", "bmm_qk"])
-def test_tcgen05_back_to_back_repeats_exact(name):
-    # C after a CUDA graph of >= 8 back-to-back launches (PDL chain, split-K
+@pytest.mark.parametrize("name,family", [("bert_ffn", "tcgen05"), ("bmm_qk", "tcgen05"),
+                                         ("conv2d", "tcgen05_conv")])
+def test_tcgen05_back_to_back_repeats_exact(name, family):
+    # C after a CUDA graph of 8 back-to-back launches (PDL chain, split-K
     # arrival tickets and in-kernel zeroing across launches) of every distinct
-    # tcgen05 configuration equals the oracle bit for bit
+    # tcgen05 GEMM / conv configuration equals the oracle bit for bit
     hdr, pop = load_population(name)
     e0 = hdr["e0"]
     progs = [p["program"] for p in pop]
@@ -88,7 +89,7 @@ def test_tcgen05_back_to_back_repeats_exact(name):
     plans = r.plan_programs(progs)
     seen = {}
     for i, p in enumerate(plans):
-        if p["family"] == "tcgen05" and p["status"] == "OK":
+        if p["family"] == family and p["status"] == "OK":
             seen.setdefault(tuple(p["cfg"]), i)
     assert seen
     for cfg, i in seen.items():
