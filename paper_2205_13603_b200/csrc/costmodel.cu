@@ -310,24 +310,29 @@ analyze_kernel(const int64_t* __restrict__ blobs, const int64_t* __restrict__ of
       int64_t red_trip = 1;
       for (int p = 0; p < nl; ++p)
         if ((((uint64_t)SR[S_RED_MASK]) >> p) & 1) red_trip *= S.ext[p];
-      Q cost;
-      if (intr) {
-        cost = qint(spec.tensor_unit_cost + SR[S_IOPEL] * spec.hit_cost);
-      } else {
-        Q am = qint(0);
-        if (SR[S_HAS_INIT]) am = qadd(am, qmk(SR[S_INIT_OPS], red_trip), &ovf);
-        if (SR[S_HAS_EPI]) am = qadd(am, qmk(SR[S_EPI_OPS], red_trip), &ovf);
-        cost = qmul(qint(spec.flop_cost), qadd(qint(SR[S_FLOPS]), am, &ovf), &ovf);
-        for (int a = 0; a < nacc; ++a) {
-          Q mf = qmk(S.mf_num[a], S.mf_den[a]);
-          Q ac = qadd(qint(spec.hit_cost), qmul(qint(spec.miss_cost - spec.hit_cost), mf, &ovf), &ovf);
-          if (S.phase[a] != 0) ac = qmul(ac, qmk(1, red_trip), &ovf);
-          cost = qadd(cost, ac, &ovf);
+      // the exact rational latency only when it is asked for (flags & 1):
+      // its int128 gcd chain is lane 0's serial critical path, and the
+      // features never read it
+      if (flags & 1) {
+        Q cost;
+        if (intr) {
+          cost = qint(spec.tensor_unit_cost + SR[S_IOPEL] * spec.hit_cost);
+        } else {
+          Q am = qint(0);
+          if (SR[S_HAS_INIT]) am = qadd(am, qmk(SR[S_INIT_OPS], red_trip), &ovf);
+          if (SR[S_HAS_EPI]) am = qadd(am, qmk(SR[S_EPI_OPS], red_trip), &ovf);
+          cost = qmul(qint(spec.flop_cost), qadd(qint(SR[S_FLOPS]), am, &ovf), &ovf);
+          for (int a = 0; a < nacc; ++a) {
+            Q mf = qmk(S.mf_num[a], S.mf_den[a]);
+            Q ac = qadd(qint(spec.hit_cost), qmul(qint(spec.miss_cost - spec.hit_cost), mf, &ovf), &ovf);
+            if (S.phase[a] != 0) ac = qmul(ac, qmk(1, red_trip), &ovf);
+            cost = qadd(cost, ac, &ovf);
+          }
         }
+        Q mult = qint(1);
+        for (int p = 0; p < nl; ++p) mult = qmul(mult, qmk(S.mult_num[enc[p]], S.mult_den[enc[p]]), &ovf);
+        total = qadd(total, qmul(cost, mult, &ovf), &ovf);
       }
-      Q mult = qint(1);
-      for (int p = 0; p < nl; ++p) mult = qmul(mult, qmk(S.mult_num[enc[p]], S.mult_den[enc[p]]), &ovf);
-      total = qadd(total, qmul(cost, mult, &ovf), &ovf);
 
       // features (`featurize` accumulation order)
       total_trip += trip;
@@ -358,8 +363,8 @@ analyze_kernel(const int64_t* __restrict__ blobs, const int64_t* __restrict__ of
   }
 
   if (lane != 0) return;
-  if (!st && ovf) st = 3;
-  if (!st && (total.n > (i128)INT64_MAX || total.d > (i128)INT64_MAX)) st = 3;
+  if ((flags & 1) && !st && ovf) st = 3;
+  if ((flags & 1) && !st && (total.n > (i128)INT64_MAX || total.d > (i128)INT64_MAX)) st = 3;
   status[prog] = st;
   if (st) return;
   if (flags & 1) { lat_num[prog] = (int64_t)total.n; lat_den[prog] = (int64_t)total.d; }
