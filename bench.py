@@ -190,6 +190,40 @@ def cpu_baseline(programs, model, budget_s=8.0):
                       f"(oracle C restatement, {threads} threads)"}
 
 
+def reference_python(texts, model_doc, sample=256):
+    """The reference's own Python on this host:
+    `_measure_batch` (`src/search.py:249-256`) with jobs=1 and jobs=#cores,
+    and `featurize` + `CostModel.predict_features` (`src/costmodel.py:21-79`,
+    `:98-102`), over a bounded sample of the slice.  Outside the timed region;
+    None when the reference package is not importable."""
+    try:
+        from paper_2205_13603_b200.refapi import loopsched
+        ls = loopsched()
+    except ImportError:
+        return None
+    import numpy as np
+    from types import SimpleNamespace
+    cores = len(os.sched_getaffinity(0))
+    progs = [ls.ir.deserialize(t) for t in texts[:sample]]
+    cands = [SimpleNamespace(program=p) for p in progs]
+    spec = ls.machine.MachineSpec()
+    out = {"sample": f"{len(progs)} programs of the slice", "cores": cores}
+    for jobs in (1, cores):
+        t0 = time.perf_counter()
+        ls.search._measure_batch(cands, spec, jobs)
+        out[f"measure_batch_jobs{jobs}_per_s"] = len(progs) / (time.perf_counter() - t0)
+    cm = ls.costmodel.CostModel(weights=np.asarray(model_doc["weights"], dtype=np.float64),
+                                intercept=float(model_doc["intercept"]),
+                                feature_mean=np.asarray(model_doc["feature_mean"], dtype=np.float64),
+                                feature_scale=np.asarray(model_doc["feature_scale"], dtype=np.float64),
+                                n_records=int(model_doc.get("n_records", 1)))
+    t0 = time.perf_counter()
+    for p in progs:
+        cm.predict_features(ls.costmodel.featurize(p, spec))
+    out["featurize_predict_per_s"] = len(progs) / (time.perf_counter() - t0)
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -424,6 +458,7 @@ def run_b200(args):
 
     if rank == 0:
         cpu = cpu_baseline(progs, model, budget_s=args.cpu_budget)
+        cpu["reference_python"] = reference_python(texts, model)
         search = reference_search(e0, dtype, local) if world == 1 and args.search_trials > 0 else None
         line = {
             "metric": METRIC, "value": total_cands / dev_s, "unit": "candidates/s", "n_gpus": world,
