@@ -54,6 +54,58 @@ struct Enc {
     return true;
   }
 
+  // An index bytecode built from constants, loop variables, +, - and
+  // products with a constant side, as c0 + sum coef * var with one term per
+  // variable OCCURRENCE (never merged).  Interval arithmetic over such a tree
+  // (`src/ir.py:394-433`) equals the sum of the per-term intervals
+  // [min(0, coef * E), max(0, coef * E)] plus c0 exactly -- scaling by a
+  // constant distributes over interval sums -- so K7 evaluates it as a short
+  // loop instead of interpreting the stack code.  Output: c0, then
+  // (position, coef) pairs.
+  static bool affine_form(const std::vector<int64_t>& ops, std::vector<int64_t>* out) {
+    struct Lin {
+      int64_t c0 = 0;
+      std::vector<std::pair<int64_t, int64_t>> t;
+    };
+    std::vector<Lin> st;
+    for (size_t i = 0; i + 1 < ops.size(); i += 2) {
+      const int64_t op = ops[i], arg = ops[i + 1];
+      if (op == BC_INT) { st.push_back(Lin{arg, {}}); continue; }
+      if (op == BC_VAR) { st.push_back(Lin{0, {{arg, 1}}}); continue; }
+      if (st.size() < 2) return false;
+      Lin b = std::move(st.back());
+      st.pop_back();
+      Lin a = std::move(st.back());
+      st.pop_back();
+      if (op == BC_SUB) {
+        b.c0 = -b.c0;
+        for (auto& q : b.t) q.second = -q.second;
+      }
+      if (op == BC_ADD || op == BC_SUB) {
+        a.c0 += b.c0;
+        a.t.insert(a.t.end(), b.t.begin(), b.t.end());
+        st.push_back(std::move(a));
+      } else if (op == BC_MUL) {
+        if (!a.t.empty() && !b.t.empty()) return false;
+        Lin& v = a.t.empty() ? b : a;
+        const int64_t k = a.t.empty() ? a.c0 : b.c0;
+        v.c0 *= k;
+        for (auto& q : v.t) q.second *= k;
+        st.push_back(std::move(v));
+      } else {
+        return false;
+      }
+    }
+    if (st.size() != 1 || st[0].t.size() > 32) return false;
+    out->clear();
+    out->push_back(st[0].c0);
+    for (const auto& q : st[0].t) {
+      out->push_back(q.first);
+      out->push_back(q.second);
+    }
+    return true;
+  }
+
   uint64_t use_mask(const std::vector<Expr*>& idx, const std::vector<Stmt*>& enc) {
     std::vector<int> vs;
     for (const Expr* e : idx) expr_vars(e, &vs);
@@ -214,8 +266,14 @@ struct Enc {
         if (!code((*x.idx)[d], enc, &ops)) return false;
         if (ops.size() / 2 > 64) return fail("index expression too long");
         size_t c = tail.size();
-        tail.push_back(static_cast<int64_t>(ops.size() / 2));
-        tail.insert(tail.end(), ops.begin(), ops.end());
+        std::vector<int64_t> lin;
+        if (affine_form(ops, &lin)) {  // [-(terms + 1), c0, (pos, coef) x terms]
+          tail.push_back(-static_cast<int64_t>((lin.size() - 1) / 2) - 1);
+          tail.insert(tail.end(), lin.begin(), lin.end());
+        } else {
+          tail.push_back(static_cast<int64_t>(ops.size() / 2));
+          tail.insert(tail.end(), ops.begin(), ops.end());
+        }
         tail[r + A_CODE + d] = static_cast<int64_t>(c);
         tail_tail_fix.push_back(r + A_CODE + d);
       }

@@ -111,9 +111,21 @@ __device__ __forceinline__ int64_t fmodp(int64_t a, int64_t b) {
 // Interval bound of one index expression (`src/ir.py:394-433`); vars of
 // enclosing positions >= t range over [0, extent-1], the rest are fixed at 0.
 __device__ bool eval_interval(const int64_t* code, const int64_t* ext, int t, int64_t* lo, int64_t* hi) {
+  int64_t n = code[0];
+  if (n < 0) {  // affine form from the encoder (costdesc.cpp affine_form): c0 + per-occurrence terms
+    int64_t l = code[1], h = code[1];
+    for (int64_t i = 0; i < -n - 1; ++i) {
+      const int64_t pos = code[2 + 2 * i], coef = code[3 + 2 * i];
+      const int64_t v = coef * (pos >= t ? ext[pos] - 1 : 0);
+      l += min(v, (int64_t)0);
+      h += max(v, (int64_t)0);
+    }
+    *lo = l;
+    *hi = h;
+    return true;
+  }
   int64_t sl[MAX_STACK], sh[MAX_STACK];
   int sp = 0;
-  int64_t n = code[0];
   for (int64_t i = 0; i < n; ++i) {
     int64_t op = code[1 + 2 * i], arg = code[2 + 2 * i];
     if (op == BC_INT) { if (sp >= MAX_STACK) return false; sl[sp] = sh[sp] = arg; ++sp; continue; }
