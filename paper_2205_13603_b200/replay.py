@@ -176,6 +176,25 @@ def _lazy_from_text(text: str, h=None):
     return p
 
 
+def serialize_trace(t) -> str:
+    """The reference's ``serialize_trace`` (`src/trace.py:82-88`), byte for
+    byte, with each instruction's JSON line cached on the (frozen, never
+    mutated) ``Instruction`` object: a mutated trace shares all but one
+    instruction with its parent (`src/trace.py:287-310` builds the changed
+    one with ``dataclasses.replace``), so re-serializing it costs one
+    ``json.dumps`` instead of one per instruction."""
+    lines = []
+    if t.workload_hash is not None:
+        lines.append(json.dumps({"workload_hash": t.workload_hash}, sort_keys=True))
+    for ins in t.instructions:
+        line = ins.__dict__.get("_ls_line")
+        if line is None:
+            line = json.dumps(ins.to_json(), sort_keys=True)
+            object.__setattr__(ins, "_ls_line", line)
+        lines.append(line)
+    return "\n".join(lines) + ("\n" if lines else "")
+
+
 def normalized_trace(key: str, text: str, t):
     """The reference's normalized trace (`src/trace.py:196-198`) from the
     native ``serialize_trace`` text, reusing the input's instruction objects
@@ -193,8 +212,10 @@ def normalized_trace(key: str, text: str, t):
             ins.append(t.instructions[k])
         else:
             d = json.loads(line)
-            ins.append(tr.Instruction(d["op"], tuple(d.get("inputs", [])), d.get("attrs", {}),
-                                      tuple(d.get("outputs", [])), d.get("decision")))
+            new_ins = tr.Instruction(d["op"], tuple(d.get("inputs", [])), d.get("attrs", {}),
+                                     tuple(d.get("outputs", [])), d.get("decision"))
+            object.__setattr__(new_ins, "_ls_line", line)  # the native line is its serialization
+            ins.append(new_ins)
     return tr.Trace(tuple(ins), workload_hash=t.workload_hash, validated=True)
 
 
@@ -285,12 +306,12 @@ def native_validator_class():
 
             def before_mutate(self, t):
                 self._building = False
-                k = getattr(t, "_ls_key", None) or ls.trace.serialize_trace(t)
+                k = getattr(t, "_ls_key", None) or serialize_trace(t)
                 if k in self._expanded:
                     return
                 keys = []
                 for m in self._pending + [t]:
-                    mk = getattr(m, "_ls_key", None) or ls.trace.serialize_trace(m)
+                    mk = getattr(m, "_ls_key", None) or serialize_trace(m)
                     if mk not in self._expanded:
                         self._expanded.add(mk)
                         keys.append(mk)
@@ -319,7 +340,7 @@ def native_validator_class():
                 return cand
 
             def candidate(self, t, model):
-                key = ls.trace.serialize_trace(t)
+                key = serialize_trace(t)
                 if key in self.cache:
                     return self._note(self._revive(self.cache[key], model))
                 (st, _idx, h, prog, norm, _reason), = self._rp.validate([key])
@@ -338,7 +359,7 @@ def native_validator_class():
                 (`src/search.py:149-159`)."""
                 key = self._keys.get(id(t))
                 if key is None or key[0] is not t:
-                    key = (t, ls.trace.serialize_trace(t))
+                    key = (t, serialize_trace(t))
                     self._keys[id(t)] = key
                 st, idx, h, prog, norm, reason = self._rp.resample(key[1], seed)
                 self.native_calls += 1
@@ -359,7 +380,7 @@ def native_validator_class():
                 native_h = getattr(program, "_ls_hash", None)
                 if not self.lookahead and native_h is None:
                     return self._note(base.from_replay(self, t, program, model))
-                key = getattr(t, "_ls_key", None) or ls.trace.serialize_trace(t)
+                key = getattr(t, "_ls_key", None) or serialize_trace(t)
                 cand = self.cache.get(key)
                 if cand is not None:
                     return self._note(self._revive(cand, model))
@@ -406,7 +427,7 @@ def native_validator_class():
                 calls that follow are cache hits (featurize stays per program)."""
                 keys, seen = [], set()
                 for t in traces:
-                    k = ls.trace.serialize_trace(t)
+                    k = serialize_trace(t)
                     if k not in self.cache and k not in seen:
                         seen.add(k)
                         keys.append((k, t))

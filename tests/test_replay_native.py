@@ -170,3 +170,32 @@ def test_lazy_program_pickles_by_text():
     p = lazy_program_class()(text)
     q = pickle.loads(pickle.dumps(p))
     assert q == p and q._ls_text == text and ls.ir.serialize(q) == text
+
+
+@needs_reference
+@pytest.mark.parametrize("name", TASKS)
+def test_cached_trace_serialization_equals_reference(name):
+    # replay.serialize_trace caches each instruction's JSON line on the
+    # instruction object; a chain of mutations (which share all but one
+    # instruction with their parent) and normalized traces rebuilt from the
+    # native text serialize byte-identically to the reference's
+    import random
+    from paper_2205_13603_b200.refapi import loopsched
+    from paper_2205_13603_b200.replay import ACCEPTED, NativeReplayer, normalized_trace, serialize_trace
+    ls = loopsched()
+    hdr, rows = load_replay(name)
+    rp = NativeReplayer(hdr["e0"])
+    rng = random.Random(7)
+    n = 0
+    for r in rows[:16]:
+        t = ls.trace.deserialize_trace(r["trace"])
+        for _ in range(12):
+            assert serialize_trace(t) == ls.trace.serialize_trace(t)
+            key = serialize_trace(t)
+            (st, _i, _h, _p, norm, _r), = rp.validate([key])
+            if st == ACCEPTED:
+                nt = normalized_trace(key, norm, t)
+                assert serialize_trace(nt) == ls.trace.serialize_trace(nt) == norm
+                n += 1
+            t, _pos = ls.trace.mutate(t, rng)
+    assert n >= 16
