@@ -165,7 +165,7 @@ def reference_search(e0_json, dtype, device, trials=64):
             t0 = time.perf_counter()
             hw = plugin.tune(e0, ls.default_space(), cfg, mode="hardware", device=device, dtype=dtype,
                              native_replay=nr, lookahead=la, min_repeats=3, max_repeats=50, target_ms=0.05,
-                             timeout_ms=5.0, timeout_factor=10.0)
+                             timeout_ms=5.0, timeout_factor=10.0, baseline_timeout_factor=2.0)
             walls.append(time.perf_counter() - t0)
         out[name] = {"wall_s": walls[1], "cold_wall_s": walls[0], "trials_per_s": len(hw.log) / walls[1],
                      "best_ns": float(hw.best_latency), "speedup_vs_e0": hw.speedup, **plugin.last_tune_stats}

@@ -171,6 +171,9 @@ ls_status ls_runner_launch_count(ls_runner* r, int64_t* count);
  * phase-B enqueue ms, [2] device spin us.  Passing n > 7 with out[7] > 0 sets
  * the per-call host cost (us) used to size the spin. */
 ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n);
+/* Change the checked-launch deadline cap (timeout_ms of the options) of later
+ * measure calls, e.g. to a multiple of the measured e0 baseline. */
+ls_status ls_runner_set_timeout(ls_runner* r, double timeout_ms);
 /* Diagnostics: launch one tcgen05 candidate `launches` times back to back
  * (one CUDA graph, PDL-chained like the timed repeats) with
  * per-CTA %globaltimer stamps (8 u64 per CTA: start, setup done, first stage

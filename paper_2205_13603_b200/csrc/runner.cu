@@ -1477,6 +1477,15 @@ ls_status ls_runner_debug_stats(ls_runner* r, double* out, int n) {
   return LS_OK;
 }
 
+ls_status ls_runner_set_timeout(ls_runner* r, double timeout_ms) {
+  if (!r || !(timeout_ms > 0.0)) {
+    set_error("ls_runner_set_timeout: bad arguments");
+    return LS_ERR_ARG;
+  }
+  r->opts.timeout_ms = timeout_ms;
+  return LS_OK;
+}
+
 void ls_runner_destroy(ls_runner* r) { delete r; }
 
 }  // extern "C"

@@ -101,6 +101,7 @@ EXPORTS = {
     "ls_runner_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, c_f32p]),
     "ls_runner_launch_count": (ctypes.c_int, [ctypes.c_void_p, c_i64p]),
     "ls_runner_debug_stats": (ctypes.c_int, [ctypes.c_void_p, c_f64p, ctypes.c_int]),
+    "ls_runner_set_timeout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
     "ls_runner_trace_tc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, c_i32p]),
     "ls_runner_destroy": (None, [ctypes.c_void_p]),

@@ -45,7 +45,8 @@ class B200Runner:
                  max_repeats: int = 200, target_ms: float = 0.2, timeout_ms: float = 2.0,
                  rtol: float = 0.0, atol: float = 0.0, sentinel_factor: float = 1e4,
                  timeout_factor: float = 0.0, timeout_floor_ms: float = 0.05,
-                 single_shot_factor: float = 0.0, carry_best: bool = False, flush_l2: bool = False):
+                 single_shot_factor: float = 0.0, carry_best: bool = False, flush_l2: bool = False,
+                 baseline_timeout_factor: float = 0.0):
         L = native.lib()
         o = native.RunnerOptsC()
         o.dtype = 1 if dtype == "bf16" else 0
@@ -63,6 +64,12 @@ class B200Runner:
         self.device = device
         self.dtype = dtype
         self.sentinel_factor = sentinel_factor
+        # > 0: once the e0 baseline is measured, the deadline cap becomes
+        # max(timeout_floor_ms, factor x baseline) (the bench's own policy:
+        # a candidate slower than 2x the unscheduled program is aborted)
+        self.baseline_timeout_factor = baseline_timeout_factor
+        self.timeout_floor_ms = timeout_floor_ms
+        self.timeout_ms = timeout_ms
         self.e0_json = None
         self._baseline = None
         self.last_results: list = []
@@ -94,6 +101,8 @@ class B200Runner:
                      "ls_runner_set_workload")
         self.e0_json = e0_json
         self._baseline = None
+        if self.baseline_timeout_factor > 0:  # back to the configured cap until e0 is re-measured
+            native.check(native.lib().ls_runner_set_timeout(self._h, self.timeout_ms), "ls_runner_set_timeout")
 
     # -- measurement ----------------------------------------------------------
     def measure_programs(self, programs: Sequence) -> list:
@@ -129,6 +138,9 @@ class B200Runner:
             if r["status"] != "OK":
                 raise native.NativeError(f"baseline e0 failed to run: {r['status']}")
             self._baseline = ns_fraction(r["latency_ns"])
+            if self.baseline_timeout_factor > 0:
+                cap = max(self.timeout_floor_ms, self.baseline_timeout_factor * r["latency_ns"] / 1e6)
+                native.check(native.lib().ls_runner_set_timeout(self._h, cap), "ls_runner_set_timeout")
         return self._baseline
 
     def sentinel(self) -> Fraction:

@@ -1,6 +1,7 @@
 """Where the wall time of a hardware-mode tune goes (native replay, the
 look-ahead's neighbour replays and batched K7, measurement, Python search):
-cProfile of plugin.tune on the GPU box, gmm512 default space, 64 trials."""
+cProfile of plugin.tune on the GPU box, default space, 64 trials:
+  python scripts/profile_search.py [gmm512|bert_ffn]"""
 import cProfile
 import json
 import pstats
@@ -14,12 +15,16 @@ from paper_2205_13603_b200.refapi import loopsched  # noqa: E402
 ls = loopsched()
 import loopsched.costmodel  # noqa: E402,F401  (scipy import outside the timing)
 
-e0 = ls.gmm(512, 512, 512)
+which = sys.argv[1] if len(sys.argv) > 1 else "gmm512"
+e0 = ls.gmm(512, 512, 512) if which == "gmm512" else ls.gmm(128, 768, 3072)
 cfg = ls.SearchConfig(trials=64, batch=16, population=64, seed=0)
-kw = dict(mode="hardware", device=0, dtype="f32", min_repeats=3, max_repeats=50, target_ms=0.05,
-          timeout_ms=5.0, timeout_factor=10.0)
+kw = dict(mode="hardware", device=0, dtype="f32" if which == "gmm512" else "bf16", min_repeats=3,
+          max_repeats=50, target_ms=0.05, timeout_ms=5.0, timeout_factor=10.0, baseline_timeout_factor=2.0)
+t0 = time.perf_counter()
+ls.tune(e0, ls.default_space(), cfg)
+print(json.dumps({"reference_cpu_wall_s": time.perf_counter() - t0}))
 plugin.tune(e0, ls.default_space(), cfg, lookahead=False, **kw)  # warm (module loads)
-for la in (False, True):
+for la in (False,) if which != "gmm512" else (False, True):
     nb = [0.0, 0]
     orig = replay.NativeReplayer.neighbours
 

@@ -431,3 +431,32 @@ def test_cold_l2_timing_mode(name):
         assert np.array_equal(cold.last_output().astype(np.float64), want)
         assert cx["latency_ns"] > 0.9 * wx["latency_ns"], (plans[i]["cfg"], cx["latency_ns"], wx["latency_ns"])
     cold.close()
+
+
+def test_baseline_relative_deadline_cap():
+    # baseline_timeout_factor: once e0 is measured, the checked-launch cap is
+    # max(timeout_floor_ms, factor x baseline); with factor 0.1 a SIMT
+    # candidate slower than that is aborted, and set_workload restores the
+    # configured cap (the naive family has no deadline checks)
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    probe = make_runner("bf16", timeout_ms=50.0)
+    probe.set_workload(e0, seed=0)
+    plans = probe.plan_programs(progs)
+    simt = pick(plans, "simt", 24)
+    res = probe.measure_programs([progs[i] for i in simt])
+    probe.close()
+    slow = [i for i, x in zip(simt, res) if x["status"] == "OK" and x["latency_ns"] > 300e3]
+    assert slow, "no SIMT candidate above 300 us in the slice"
+    r = make_runner("bf16", timeout_ms=50.0, baseline_timeout_factor=0.1, timeout_floor_ms=0.05)
+    r.set_workload(e0, seed=0)
+    base_ns = float(r.baseline())
+    cap_ns = max(50e3, 0.1 * base_ns)
+    x, = r.measure_programs([progs[slow[0]]])
+    assert x["status"] == "TIMEOUT", x
+    assert x["latency_ns"] < 300e3 and x["latency_ns"] > 0.5 * cap_ns
+    r.set_workload(e0, seed=0)
+    y, = r.measure_programs([progs[slow[0]]])
+    assert y["status"] == "OK" and y["mismatches"] == 0, y
+    r.close()
