@@ -289,6 +289,23 @@ def installed(runner=None, scorer=None, exact_scores: bool = False, native_repla
 last_tune_stats: dict = {}
 
 
+_RUNNER_POOL: dict = {}
+
+
+def _pooled_runner(device, dtype, opts):
+    """One hardware runner per (device, dtype, options), reused across tunes:
+    creating one costs milliseconds (kernel preloads, pinned staging) and
+    destroying one ~0.1 s (device and pinned frees), which would otherwise
+    land inside the next tune's wall time.  ``set_workload`` resets the
+    per-workload state (reference output, baseline, deadline cap)."""
+    from .runner import B200Runner
+    key = (device, dtype, tuple(sorted(opts.items())))
+    r = _RUNNER_POOL.get(key)
+    if r is None or getattr(r, "_h", None) is None:
+        r = _RUNNER_POOL[key] = B200Runner(device=device, dtype=dtype, **opts)
+    return r
+
+
 def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
          mode: str = "hardware", runner=None, scorer=None, device: int = 0, dtype: str = "bf16",
          native_replay: bool = True, lookahead: bool = False, **runner_opts):
@@ -307,8 +324,7 @@ def tune(e0, generator, config=None, machine_spec=None, warm_records=None, *,
         if mode == "parity":
             runner = SimRunner(device, scorer)
         elif mode == "hardware":
-            from .runner import B200Runner
-            runner = B200Runner(device=device, dtype=dtype, **runner_opts)
+            runner = _pooled_runner(device, dtype, runner_opts)
             runner.set_workload(e0)
         else:
             raise ValueError(f"unknown mode {mode!r}")
