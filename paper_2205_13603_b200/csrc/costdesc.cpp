@@ -131,22 +131,31 @@ struct Enc {
     } else {
       for (const auto& ix : s->op_indices) lists.push_back(&ix);
     }
+    // per index list, once: its variables, the variables of every dimension
+    // but the last, and the last dimension's affine coefficients; then each
+    // enclosing position is a few lookups
+    struct ListInfo {
+      std::vector<int> all, lead;
+      bool affine = false;
+      std::vector<int64_t> coeff;
+    };
+    std::vector<ListInfo> info(lists.size());
+    for (size_t k = 0; k < lists.size(); ++k) {
+      const auto* ix = lists[k];
+      ListInfo& li = info[k];
+      for (const Expr* e : *ix) expr_vars(e, &li.all);
+      for (size_t d = 0; d + 1 < ix->size(); ++d) expr_vars((*ix)[d], &li.lead);
+      int64_t c0;
+      li.affine = !ix->empty() && affine_coeffs(ix->back(), p.vars.size(), &li.coeff, &c0);
+    }
     uint64_t ok = 0;
     for (size_t pos = 0; pos < enc.size(); ++pos) {
       int v = enc[pos]->var;
       bool good = true;
-      for (const auto* ix : lists) {
-        std::vector<int> vs;
-        for (const Expr* e : *ix) expr_vars(e, &vs);
-        if (std::find(vs.begin(), vs.end(), v) == vs.end()) continue;
-        for (size_t d = 0; d + 1 < ix->size(); ++d) {
-          std::vector<int> vd;
-          expr_vars((*ix)[d], &vd);
-          if (std::find(vd.begin(), vd.end(), v) != vd.end()) good = false;
-        }
-        std::vector<int64_t> coeff;
-        int64_t c0;
-        if (ix->empty() || !affine_coeffs(ix->back(), p.vars.size(), &coeff, &c0) || coeff[v] != 1) good = false;
+      for (const ListInfo& li : info) {
+        if (std::find(li.all.begin(), li.all.end(), v) == li.all.end()) continue;
+        if (std::find(li.lead.begin(), li.lead.end(), v) != li.lead.end()) good = false;
+        if (!li.affine || li.coeff[v] != 1) good = false;
         if (!good) break;
       }
       if (good) ok |= 1ull << pos;
