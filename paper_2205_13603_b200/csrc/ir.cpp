@@ -89,14 +89,17 @@ class Reader {
   }
   bool integer(int64_t* v) {
     ws();
-    const char* b = s_.data() + i_;
-    char* e = nullptr;
-    long long x = std::strtoll(b, &e, 10);
-    if (e == b) return fail("expected integer");
-    if (static_cast<size_t>(e - s_.data()) < s_.size() && (*e == '.' || *e == 'e' || *e == 'E'))
-      return fail("non-integer number");
-    i_ = static_cast<size_t>(e - s_.data());
-    *v = x;
+    size_t j = i_;
+    const bool neg = j < s_.size() && s_[j] == '-';
+    if (neg) ++j;
+    const size_t d0 = j;
+    uint64_t x = 0;
+    while (j < s_.size() && s_[j] >= '0' && s_[j] <= '9' && j - d0 < 19) x = x * 10 + static_cast<uint64_t>(s_[j++] - '0');
+    if (j == d0) return fail("expected integer");
+    if (j < s_.size() && (s_[j] == '.' || s_[j] == 'e' || s_[j] == 'E' || (s_[j] >= '0' && s_[j] <= '9')))
+      return fail("non-integer number");  // fractions, exponents, more than 18 digits
+    i_ = j;
+    *v = neg ? -static_cast<int64_t>(x) : static_cast<int64_t>(x);
     return true;
   }
   bool skip_value() {
@@ -181,13 +184,15 @@ class Reader {
     });
   }
 
-  int var_id(const std::string& name) {
+  // names (loop variables, buffers) carry no escapes in the interchange
+  // format, so they are read as views (key()) and only copied when new
+  int var_id(std::string_view name) {
     for (size_t i = 0; i < p_->vars.size(); ++i)
       if (p_->vars[i] == name) return static_cast<int>(i);
-    p_->vars.push_back(name);
+    p_->vars.emplace_back(name);
     return static_cast<int>(p_->vars.size()) - 1;
   }
-  int buf_id(const std::string& name) {
+  int buf_id(std::string_view name) {
     int b = p_->buffer_id(name);
     if (b < 0) fail("unknown buffer");
     return b;
@@ -200,15 +205,13 @@ class Reader {
 
   Expr* expr() {
     Expr* e = p_->new_expr();
-    std::string tag;
     bool ok = object([&](std::string_view k) {
-      tag = k;
       if (k == "int") { e->op = Op::Int; return integer(&e->value); }
-      if (k == "var") { std::string n; if (!string(&n)) return false; e->op = Op::Var; e->var = var_id(n); return true; }
+      if (k == "var") { std::string_view n; if (!key(&n)) return false; e->op = Op::Var; e->var = var_id(n); return true; }
       if (k == "load") {
         e->op = Op::Load;
         return object([&](std::string_view lk) {
-          if (lk == "buffer") { std::string n; if (!string(&n)) return false; e->buffer = buf_id(n); return good(); }
+          if (lk == "buffer") { std::string_view n; if (!key(&n)) return false; e->buffer = buf_id(n); return good(); }
           if (lk == "indices") return expr_list(&e->kids);
           return skip_value();
         });
@@ -235,7 +238,7 @@ class Reader {
       if (k == "loop") {
         s->type = SType::Loop;
         return object([&](std::string_view lk) {
-          if (lk == "var") { std::string n; if (!string(&n)) return false; s->var = var_id(n); return true; }
+          if (lk == "var") { std::string_view n; if (!key(&n)) return false; s->var = var_id(n); return true; }
           if (lk == "extent") return integer(&s->extent);
           if (lk == "kind") {
             std::string kd;
@@ -255,7 +258,7 @@ class Reader {
         s->type = SType::Compute;
         return object([&](std::string_view ck) {
           if (ck == "name") return string(&s->name);
-          if (ck == "buffer") { std::string n; if (!string(&n)) return false; s->buffer = buf_id(n); return good(); }
+          if (ck == "buffer") { std::string_view n; if (!key(&n)) return false; s->buffer = buf_id(n); return good(); }
           if (ck == "indices") return expr_list(&s->indices);
           if (ck == "value") return (s->value = expr()) != nullptr;
           if (ck == "init") return (s->init = expr()) != nullptr;
@@ -283,7 +286,7 @@ class Reader {
               int buf = -1;
               std::vector<Expr*> idx;
               bool r = object([&](std::string_view ok2) {
-                if (ok2 == "buffer") { std::string n; if (!string(&n)) return false; buf = buf_id(n); return good(); }
+                if (ok2 == "buffer") { std::string_view n; if (!key(&n)) return false; buf = buf_id(n); return good(); }
                 if (ok2 == "indices") return expr_list(&idx);
                 return skip_value();
               });
