@@ -25,6 +25,8 @@ exit even when the search raises.
 
 from __future__ import annotations
 
+import atexit
+
 import contextlib
 import threading
 from fractions import Fraction
@@ -290,6 +292,17 @@ last_tune_stats: dict = {}
 
 
 _RUNNER_POOL: dict = {}
+
+
+def close_runner_pool() -> None:
+    """Destroy the pooled hardware runners (also run at interpreter exit,
+    before the CUDA context is torn down)."""
+    while _RUNNER_POOL:
+        _, r = _RUNNER_POOL.popitem()
+        r.close()
+
+
+atexit.register(close_runner_pool)
 
 
 def _pooled_runner(device, dtype, opts):
