@@ -26,7 +26,6 @@ exit even when the search raises.
 from __future__ import annotations
 
 import atexit
-
 import contextlib
 import threading
 from fractions import Fraction
