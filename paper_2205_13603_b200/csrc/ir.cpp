@@ -102,16 +102,27 @@ class Reader {
     *v = neg ? -static_cast<int64_t>(x) : static_cast<int64_t>(x);
     return true;
   }
+  // a string skipped in place (no copy): the first pass over the root and
+  // unknown keys only need its end
+  bool skip_string() {
+    ws();
+    if (i_ >= s_.size() || s_[i_] != '"') return fail("expected string");
+    ++i_;
+    while (i_ < s_.size() && s_[i_] != '"') i_ += s_[i_] == '\\' ? 2 : 1;
+    if (i_ >= s_.size()) return fail("unterminated string");
+    ++i_;
+    return true;
+  }
   bool skip_value() {
     char c = peek();
-    if (c == '"') { std::string t; return string(&t); }
+    if (c == '"') return skip_string();
     if (c == '{' || c == '[') {
       char close = c == '{' ? '}' : ']';
       ++i_;
       for (bool first = true;; first = false) {
         if (peek() == close) { ++i_; return true; }
         if (!first && !expect(',')) return false;
-        if (c == '{') { std::string k; if (!string(&k) || !expect(':')) return false; }
+        if (c == '{' && (!skip_string() || !expect(':'))) return false;
         if (!skip_value()) return false;
       }
     }

@@ -170,8 +170,26 @@ def check(status: int, what: str) -> None:
 
 
 def text_array(programs):
+    """(const char* const*, const size_t*, keep-alive) for a list of program /
+    trace texts.  Large batches are joined into one buffer and the pointer
+    array is built with numpy (creating one ``c_char_p`` per text costs more
+    than the native call's parsing for 1k programs); texts must then be ASCII
+    (the reference writes JSON with ``ensure_ascii``), else per-text encoding."""
+    n = len(programs)
+    if n >= 64 and all(isinstance(p, str) for p in programs):
+        lens = np.fromiter(map(len, programs), dtype=np.uint64, count=n)
+        try:
+            b = "".join(programs).encode("ascii")
+        except UnicodeEncodeError:
+            b = None
+        if b is not None:
+            buf = np.frombuffer(b, dtype=np.uint8)
+            off = np.zeros(n, dtype=np.uint64)
+            np.cumsum(lens[:-1], out=off[1:])
+            ptrs = off + np.uint64(buf.ctypes.data)
+            return (ptrs.ctypes.data_as(ctypes.POINTER(ctypes.c_char_p)),
+                    lens.ctypes.data_as(ctypes.POINTER(ctypes.c_size_t)), (b, buf, ptrs, lens))
     enc = [p.encode() if isinstance(p, str) else bytes(p) for p in programs]
-    n = len(enc)
     arr = (ctypes.c_char_p * max(n, 1))(*enc)
     lens = (ctypes.c_size_t * max(n, 1))(*[len(b) for b in enc])
     return arr, lens, enc
