@@ -1,8 +1,9 @@
-"""compute-sanitizer driver: one tcgen05 GEMM candidate per split-K mode
-(mode 0: no split; mode 2: arrival ticket + in-kernel zeroing + TMA
-add-reduce), one tcgen05 bmm and one tcgen05 conv per mode, each measured a
-few times through the Runner (checked launch + timed repeats), outputs
-compared with the fp64 reference run.  Run as
+"""compute-sanitizer driver: one tcgen05 GEMM / bmm / conv candidate per
+kernel instantiation the population reaches -- split-K mode (0: no split; 2:
+arrival ticket + in-kernel zeroing + add-reduce) x epilogue (register-direct
+for unsplit BN <= 32, TMA store / add-reduce for BN % 32 == 0, staged
+otherwise) -- each measured a few times through the Runner (checked launch +
+timed repeats), outputs compared with the fp64 reference run.  Run as
   compute-sanitizer --tool {memcheck,racecheck,synccheck} python scripts/sanitize_tc.py
 """
 import gzip
@@ -25,7 +26,8 @@ def load(name):
 
 def main():
     bad = 0
-    for name, fam, cfg_split in (("bert_ffn", "tcgen05", 4), ("bmm_qk", "tcgen05", 4), ("conv2d", "tcgen05_conv", 3)):
+    for name, fam, cfg_split, cfg_bn in (("bert_ffn", "tcgen05", 4, 3), ("bmm_qk", "tcgen05", 4, 3),
+                                         ("conv2d", "tcgen05_conv", 3, 2)):
         e0, progs = load(name)
         r = B200Runner(device=0, dtype="bf16", min_repeats=2, max_repeats=2, target_ms=0.001, timeout_ms=60000.0)
         r.set_workload(e0, seed=0)
@@ -35,9 +37,12 @@ def main():
         for i, p in enumerate(plans):
             if p["family"] != fam or p["status"] != "OK":
                 continue
-            split = p["cfg"][cfg_split]
-            mode = "split" if split > 1 else "nosplit"
-            picks.setdefault(mode, i)
+            split, bn = p["cfg"][cfg_split], p["cfg"][cfg_bn]
+            if fam == "tcgen05" and split == 1 and bn <= 32:
+                epi = "direct"
+            else:
+                epi = "tma" if bn % 32 == 0 else "staged"
+            picks.setdefault(("split" if split > 1 else "nosplit") + "/" + epi, i)
         for mode, i in sorted(picks.items()):
             res, = r.measure_programs([progs[i]])
             out = r.last_output().astype(np.float64)
