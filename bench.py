@@ -38,6 +38,7 @@ WORKLOADS = {
     "bert_ffn": ("pop_bert_ffn.jsonl.gz", "bf16", "BERT-base dense GEMM 128x768x3072 bf16 with tcgen05 tensorize"),
     "bmm_qk": ("pop_bmm_qk.jsonl.gz", "bf16", "BERT-base attention batch_matmul 12x128x128x64 bf16"),
     "gmm512": ("pop_gmm512.jsonl.gz", "f32", "GEMM 512x512x512 fp32"),
+    "gmm512_tc": ("pop_gmm512_tc.jsonl.gz", "f32", "GEMM 512x512x512 fp32 with tcgen05 tensorize (3xTF32)"),
     "conv2d": ("pop_conv2d.jsonl.gz", "bf16", "ResNet-50 conv2d 56x56x64->64 3x3 NHWC bf16 implicit GEMM"),
 }
 
@@ -393,7 +394,13 @@ def run_b200(args):
             best, best_text = rem[j], texts[top[j]]
     peak_bf16, peak_hbm, peak_src = peaks()
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-    peak = peak_bf16 if dtype == "bf16" else fp32_peak
+    # an fp32 tcgen05 tile runs as 3xTF32: three kind::tf32 passes at half the
+    # bf16 rate, so its roof is bf16 / 6 in fp32 FLOP/s
+    x3 = dtype != "bf16" and best is not None and best["family"] == "tcgen05"
+    peak = peak_bf16 if dtype == "bf16" else peak_bf16 / 6 if x3 else fp32_peak
+    bound = "tensor" if dtype == "bf16" else "tensor (3xTF32)" if x3 else "fp32-simt"
+    peak_note = (peak_src if dtype == "bf16" else
+                 f"{peak_src} bf16 / 6 (tf32 = bf16 / 2, three passes)" if x3 else "fp32 SIMT nominal")
     best_tflops = flops / (best["latency_ns"] * 1e-9) / 1e12 if best else None
     from collections import Counter
     fam = Counter((r["family"], r["status"]) for r in results[-1])
@@ -490,7 +497,7 @@ def run_b200(args):
             "clocks": clk,
             "best_schedule": None if best is None else {
                 "tflops": best_tflops, "frac_of_peak": best_tflops / peak,
-                "peak": peak, "peak_source": peak_src if dtype == "bf16" else "fp32 SIMT nominal",
+                "peak": peak, "peak_source": peak_note,
                 "latency_us": best["latency_ns"] / 1e3, "isolated_us": isolated_us,
                 "cold_l2_us": cold_us,
                 "family": best["family"], "cfg": best["cfg"],
@@ -510,7 +517,8 @@ def run_b200(args):
             "outcomes": {f"{a}/{b}": c for (a, b), c in sorted(fam.items())},
             "outcome_device_ms": {f"{a}/{b}": round(v, 3) for (a, b), v in sorted(fam_ms.items())},
             "roofline": None if best is None else {
-                "bound": "tensor" if dtype == "bf16" else "fp32-simt", "achieved": best_tflops,
+                "bound": bound, "achieved": best_tflops,
+                "frac_of_fp32_simt_peak": None if dtype == "bf16" else best_tflops / fp32_peak,
                 "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
                 "traffic": traffic_bytes, "traffic_source": traffic_src,
                 "frac_isolated": None if not isolated_us else flops / (isolated_us * 1e-6) / 1e12 / peak,

@@ -197,6 +197,46 @@ __global__ void transpose_kernel(const __nv_bfloat16* __restrict__ in, __nv_bflo
   }
 }
 
+// 3xTF32 operand split: hi = x rounded to the nearest tf32 (10 mantissa
+// bits), lo = x - hi (exact in fp32, |lo| <= 2^-11 |x|) rounded to the
+// nearest tf32 as well, so the tensor core's own reduction of its inputs to
+// tf32 drops nothing; hi + lo carries ~22 significant bits of x.
+// out[0][b][c][r] = hi, out[1][b][c][r] = lo of in[b][r][c] when transposing,
+// of in[b][c][r] otherwise.  Small integers split as (x, 0): exact.
+__device__ __forceinline__ float round_tf32(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void tf32_split(float x, float* hi, float* lo) {
+  const float h = round_tf32(x);
+  *hi = h;
+  *lo = round_tf32(x - h);
+}
+
+__global__ void split_tf32_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t rows, int64_t cols,
+                                  int64_t lo_off, bool transpose) {
+  __shared__ float tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const float* src = in + b * rows * cols;
+  float* dst = out + b * rows * cols;
+  if (!transpose) {
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t r = r0 + i, cc = c0 + threadIdx.x;
+      if (r < rows && cc < cols) tf32_split(src[r * cols + cc], dst + r * cols + cc, dst + lo_off + r * cols + cc);
+    }
+    return;
+  }
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, cc = c0 + threadIdx.x;
+    if (r < rows && cc < cols) tile[i][threadIdx.x] = src[r * cols + cc];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t cc = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && cc < cols) tf32_split(tile[threadIdx.x][i], dst + cc * rows + r, dst + lo_off + cc * rows + r);
+  }
+}
+
 }  // namespace
 
 int opt_in_dynamic_smem(const void* fn) {
@@ -366,6 +406,12 @@ void launch_transpose_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t 
                            cudaStream_t st) {
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+}
+
+void launch_split_tf32(const float* in, float* out, int64_t batch, int64_t rows, int64_t cols, bool transpose,
+                       cudaStream_t st) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32), (unsigned)batch);
+  split_tf32_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols, batch * rows * cols, transpose);
 }
 
 }  // namespace lsb

@@ -46,6 +46,10 @@ void launch_delay(unsigned long long ns, cudaStream_t st);
 void launch_gate(const unsigned int* flag, unsigned int want, unsigned long long max_ns, cudaStream_t st);
 // fp32 -> bf16 copy, and an optional 2-D transpose to make K contiguous
 void launch_to_bf16(const float* in, __nv_bfloat16* out, int64_t n, cudaStream_t st);
+// 3xTF32 operands of an fp32 contraction: out = [hi | lo] ([2][batch][..]),
+// each [batch][cols][rows] (transpose) or [batch][rows][cols] (copy) of in
+void launch_split_tf32(const float* in, float* out, int64_t batch, int64_t rows, int64_t cols, bool transpose,
+                       cudaStream_t st);
 void launch_transpose_bf16(const __nv_bfloat16* in, __nv_bfloat16* out, int64_t batch, int64_t rows,
                            int64_t cols, cudaStream_t st);
 
@@ -71,6 +75,7 @@ struct TcLaunch {
   unsigned long long* trace = nullptr;  // optional per-CTA timeline (8 stamps per CTA)
   uint32_t* sync = nullptr;             // split-K ticket slots of this candidate (2 x kTcSyncSlots, zeroed)
   bool pdl = true;                      // programmatic dependent launch
+  bool x3 = false;  // fp32 operands as 3xTF32: tmap_a / tmap_b cover [hi | lo] (2 x batch), kt in 64-element tiles
 };
 bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st);
 

@@ -185,7 +185,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
         ++nonserial;
         at = i;
       }
-    if (nonserial == 1 && lim.bf16 && parts[at].kind == Kind::Unrolled && parts[at].role == R_K &&
+    if (nonserial == 1 && (lim.bf16 || lim.tf32x3) && parts[at].kind == Kind::Unrolled && parts[at].role == R_K &&
         at + 1 < parts.size() && parts[at + 1].role == R_M) {
       traced_stages = parts[at].extent;
       parts[at].kind = Kind::Serial;
@@ -237,7 +237,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
 
   // ---- TCGEN05: innermost [M 128][N BN][K 64] tile --------------------------
   size_t np = merged.size();
-  if (lim.bf16 && np >= 3) {
+  if ((lim.bf16 || lim.tf32x3) && np >= 3) {
     const Part& pm = merged[np - 3];
     const Part& pn = merged[np - 2];
     const Part& pk = merged[np - 1];
@@ -251,6 +251,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       t.grid_n = w.extent[R_N] / t.bn;
       t.splits = 1;
       t.kt = 1;
+      t.x3 = !lim.bf16;
       bool before_spatial = true;
       for (size_t i = 0; i + 3 < np; ++i) {
         if (merged[i].role != R_K) { before_spatial = false; continue; }
@@ -260,12 +261,15 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       // stage count: the traced pipeline depth, or as many k-tiles as fit in
       // shared memory (<= 8)
       const int64_t tiles = t.batch * t.grid_m * t.grid_n;
-      const TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles);
+      // (3xTF32 ring slots are 32-element k sub-tiles: two per k-tile)
+      const int64_t per_kt = t.x3 ? 2 : 1;
+      const TcGeom g0 = tc_geom(t.bn, t.splits, 1, tiles, t.x3);
       const int64_t avail = lim.max_smem - 1024 - 256;
       const int64_t fit = std::max<int64_t>(1, avail / g0.stage_bytes);
-      t.stages = traced_stages ? std::min(traced_stages, t.kt) : std::min<int64_t>({t.kt, fit, 8});
-      if (traced_stages > fit) return illegal(plan, "traced pipeline depth above shared memory");
-      const TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles);
+      const int64_t slots = per_kt * t.kt;
+      t.stages = traced_stages ? std::min(per_kt * traced_stages, slots) : std::min<int64_t>({slots, fit, 8});
+      if (per_kt * traced_stages > fit) return illegal(plan, "traced pipeline depth above shared memory");
+      const TcGeom g = tc_geom(t.bn, t.splits, t.stages, tiles, t.x3);
       plan.needs_zero = g.mode == 3;
       t.smem_bytes = g.smem;
       int32_t* c = plan.cfg;
@@ -273,6 +277,7 @@ Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim) 
       c[2] = static_cast<int32_t>(t.grid_n); c[3] = static_cast<int32_t>(t.bn);
       c[4] = static_cast<int32_t>(t.splits); c[5] = static_cast<int32_t>(t.kt);
       c[6] = static_cast<int32_t>(t.stages); c[7] = static_cast<int32_t>(t.smem_bytes / 1024);
+      c[8] = t.x3 ? 1 : 0;
       if (t.bn > 256) return illegal(plan, "UMMA N above 256");
       if (t.smem_bytes > lim.max_smem) return illegal(plan, "shared-memory ring + reduction buffer above 227 KB");
       if (t.batch * t.splits > 65535 || t.grid_m > 65535) return illegal(plan, "grid too large");

@@ -13,7 +13,8 @@
 //   * innermost parts [M 128][N 16..256][K 64] with bf16 data -> TCGEN05:
 //     one UMMA tile per CTA, K parts hoisted above every spatial loop become
 //     split-K, the other outer K parts the k-tile pipeline, spatial parts the
-//     grid;
+//     grid; with fp32 data the same tile runs as 3xTF32 (hi/lo operand
+//     halves, three kind::tf32 UMMAs per k step, fp32-accurate);
 //   * otherwise                            -> SIMT: spatial part 0 -> grid,
 //     part 1 -> threads, parts >= 2 -> per-thread register tile; innermost K
 //     part -> shared-memory k-tile (BK), outer K parts -> k-tile loop.
@@ -69,7 +70,8 @@ struct SimtCfg {
 
 struct TcCfg {
   int64_t bn, splits, kt, grid_m, grid_n, batch;
-  int64_t stages, smem_bytes;
+  int64_t stages, smem_bytes;  // stages: ring slots (3xTF32: 32-element k sub-tiles, two per k-tile)
+  bool x3 = false;              // fp32 workload: 3xTF32 operand halves
 };
 
 // Split-K reduction of the TCGEN05 family and the shared-memory layout it
@@ -92,10 +94,11 @@ struct TcGeom {
   bool tma_epi = false;     // BN % 32 == 0: 128B-swizzled 32-column chunks, TMA store / add-reduce
   bool direct = false;      // mode 0, BN <= 32: TMEM -> registers -> global, no staging
   int ld = 0;               // padded fp32 row of the staged tile (generic epilogue)
-  int64_t stage_bytes = 0;  // one k-tile: A 128x64 + B BNx64 bf16
+  int64_t stage_bytes = 0;  // one stage: A 128 rows + B BN rows of 128 bytes (bf16 k-tile of 64;
+                            // 3xTF32: hi and lo of a 32-element fp32 k sub-tile, twice the bytes)
   int64_t ring = 0, tile = 0, smem = 0;
 };
-inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles) {
+inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles, bool x3 = false) {
   TcGeom g;
   g.mode = splits == 1 ? 0 : tiles <= kTcSyncSlots ? 2 : 3;
   // no split and a narrow tile: each thread stores its TMEM row straight from
@@ -103,7 +106,7 @@ inline TcGeom tc_geom(int64_t bn, int64_t splits, int64_t stages, int64_t tiles)
   g.direct = g.mode == 0 && bn <= 32;
   g.tma_epi = bn % 32 == 0 && g.mode != 3 && !g.direct;
   g.ld = static_cast<int>(bn + 4);  // padded fp32 row (16-byte aligned, conflict-free)
-  g.stage_bytes = 128 * 64 * 2 + bn * 64 * 2;
+  g.stage_bytes = (128 * 64 * 2 + bn * 64 * 2) * (x3 ? 2 : 1);
   g.ring = stages * g.stage_bytes;
   // staged accumulator tile, overlays the finished ring
   g.tile = g.direct ? 0 : g.tma_epi ? (bn / 32) * 16384 : 128LL * g.ld * 4;
@@ -135,7 +138,8 @@ struct Plan {
 struct DeviceLimits {
   int64_t max_threads = 1024;
   int64_t max_smem = 227 * 1024;
-  bool bf16 = false;  // runner dtype
+  bool bf16 = false;    // runner dtype bf16 and the tcgen05 operand layout available
+  bool tf32x3 = false;  // runner dtype fp32 and the 3xTF32 operand halves available
 };
 
 Plan plan_program(const Workload& w, const Program& p, const DeviceLimits& lim);

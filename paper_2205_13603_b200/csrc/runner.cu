@@ -61,16 +61,20 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// bf16 K-major operand [batch][rows][K] as a 3-D TMA map with a {64, box_rows, 1} box.
-bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, int64_t k, int box_rows) {
+// K-major operand [batch][rows][K] as a 3-D TMA map whose box is one
+// 128-byte swizzle row per operand row: {64, box_rows, 1} of bf16, or
+// {32, box_rows, 1} of fp32 (the 3xTF32 halves; batch then counts hi and lo).
+bool make_kmajor_map(CUtensorMap* map, void* base, int64_t batch, int64_t rows, int64_t k, int box_rows,
+                     bool f32 = false) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
+  const int64_t es = f32 ? 4 : 2;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * 2), static_cast<cuuint64_t>(rows * k * 2)};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k * es), static_cast<cuuint64_t>(rows * k * es)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -148,7 +152,8 @@ struct ls_runner {
   bool tc_ok = false;
   void* x = nullptr;        // device inputs in the runner dtype
   void* y = nullptr;
-  void* yk = nullptr;       // K-major copy of Y for the tcgen05 family (bf16)
+  void* yk = nullptr;       // K-major copy of Y for the tcgen05 family (bf16; fp32: [hi | lo] halves)
+  void* xs = nullptr;       // fp32 workloads: [hi | lo] halves of X for the 3xTF32 tcgen05 tile
   float* c = nullptr;
   double* ref = nullptr;
   Strides s{};
@@ -220,8 +225,8 @@ struct ls_runner {
     tmap_o.clear();
     gbuf_dtype.clear();
     general = false;
-    pfree(x); pfree(y); pfree(yk); pfree(c); pfree(ref);
-    x = y = yk = nullptr; c = nullptr; ref = nullptr;
+    pfree(x); pfree(y); pfree(yk); pfree(xs); pfree(c); pfree(ref);
+    x = y = yk = xs = nullptr; c = nullptr; ref = nullptr;
     tmap_b.clear();
     tmap_am.clear();
     have_tmap_c = false;
@@ -273,7 +278,9 @@ struct ls_runner {
     auto it = tmap_am.find(rows);
     if (it != tmap_am.end()) return &it->second;
     CUtensorMap m;
-    if (!make_kmajor_map(&m, x, w.extent[R_BATCH], w.extent[R_M], w.extent[R_K], rows)) return nullptr;
+    const int64_t halves = bf16 ? 1 : 2;
+    if (!make_kmajor_map(&m, bf16 ? x : xs, halves * w.extent[R_BATCH], w.extent[R_M], w.extent[R_K], rows, !bf16))
+      return nullptr;
     return &(tmap_am[rows] = m);
   }
   const CUtensorMap* map_b(int bn) {
@@ -281,7 +288,8 @@ struct ls_runner {
     auto it = tmap_b.find(bn);
     if (it != tmap_b.end()) return &it->second;
     CUtensorMap m;
-    if (!make_kmajor_map(&m, yk, w.extent[R_BATCH], w.extent[R_N], w.extent[R_K], bn)) return nullptr;
+    const int64_t halves = bf16 ? 1 : 2;
+    if (!make_kmajor_map(&m, yk, halves * w.extent[R_BATCH], w.extent[R_N], w.extent[R_K], bn, !bf16)) return nullptr;
     return &(tmap_b[bn] = m);
   }
 
@@ -306,7 +314,7 @@ struct ls_runner {
         if (!want) continue;
       } else {
         if (p.family != F_TC) continue;
-        if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n).mode != 2)
+        if (tc_geom(p.tc.bn, p.tc.splits, p.tc.stages, p.tc.batch * p.tc.grid_m * p.tc.grid_n, p.tc.x3).mode != 2)
           continue;
       }
       sync_off[i] = static_cast<int64_t>(words);
@@ -464,6 +472,7 @@ struct ls_runner {
         L.grid_n = static_cast<int>(p.tc.grid_n);
         L.smem_bytes = static_cast<int>(p.tc.smem_bytes);
         L.trace = trace;
+        L.x3 = p.tc.x3;
         L.sync = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
                      ? tcsync + sync_off[static_cast<size_t>(slot)]
                      : nullptr;
@@ -511,6 +520,7 @@ ls_status plan_all(const Workload& w, const GeneralWorkload* gw, const DeviceLim
     if (out.status == P_UNSUPPORTED && alt) {
       DeviceLimits la = lim;
       la.bf16 = false;  // no tcgen05 conv for a plain contraction
+      la.tf32x3 = false;
       auto g = std::make_shared<GeneralPlan>(plan_general(*alt, *p, la));
       if (g->status == P_OK) {
         out = Plan();
@@ -620,6 +630,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
   // weight viewed as [k_rows][n_cols] (n = its contiguous last dim)
   r->tc_ok = false;
   r->lim.bf16 = false;
+  r->lim.tf32x3 = false;
   for (size_t b = 0; b < nb && r->bf16; ++b) {
     if (gw.buffers[b] != gw.y_buf || gw.roles[b] != 0) continue;
     const std::vector<int64_t>& sh = gw.shapes[b];
@@ -668,6 +679,7 @@ ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* pro
   }
   DeviceLimits lim;
   lim.bf16 = !general && dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
+  lim.tf32x3 = !general && dtype != LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
   if (general && dtype == LS_DTYPE_BF16)
     for (size_t b = 0; b < gw.buffers.size(); ++b)
       if (gw.buffers[b] == gw.y_buf && gw.roles[b] == 0) {
@@ -846,14 +858,27 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
   LSB_CUDA(cudaGetLastError());
 
   // tcgen05 operands: X must be [batch][M][K]; Y is used K-major ([batch][N][K]),
-  // transposed once here when the workload stores it [batch][K][N].
+  // transposed once here when the workload stores it [batch][K][N].  fp32
+  // workloads get both as [hi | lo] halves for the 3xTF32 tile.
   const int64_t B = w.extent[R_BATCH], M = w.extent[R_M], N = w.extent[R_N], K = w.extent[R_K];
   bool x_ok = w.x_kmajor && w.sx[R_M] == K && (!w.has_batch || w.sx[R_BATCH] == M * K);
   bool y_kmaj = w.y_kmajor && w.sy[R_N] == K && (!w.has_batch || w.sy[R_BATCH] == N * K);
   bool y_nmaj = !w.y_kmajor && w.sy[R_N] == 1 && w.sy[R_K] == N && (!w.has_batch || w.sy[R_BATCH] == N * K);
   bool c_ok = w.sc[R_N] == 1 && w.sc[R_M] == N && (!w.has_batch || w.sc[R_BATCH] == M * N);
-  r->tc_ok = r->bf16 && x_ok && (y_kmaj || y_nmaj) && c_ok && K % 64 == 0 && M % 128 == 0;
-  if (r->tc_ok) {
+  r->tc_ok = x_ok && (y_kmaj || y_nmaj) && c_ok && K % 64 == 0 && M % 128 == 0;
+  if (r->tc_ok && !r->bf16) {
+    LSB_CUDA(r->pmalloc(&r->xs, static_cast<size_t>(w.x_elems) * 8));
+    LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 8));
+    launch_split_tf32(static_cast<const float*>(r->x), static_cast<float*>(r->xs), B, M, K, false, r->st);
+    if (y_kmaj) launch_split_tf32(static_cast<const float*>(r->y), static_cast<float*>(r->yk), B, N, K, false, r->st);
+    else launch_split_tf32(static_cast<const float*>(r->y), static_cast<float*>(r->yk), B, K, N, true, r->st);
+    LSB_CUDA(cudaGetLastError());
+    if (!make_kmajor_map(&r->tmap_a, r->xs, 2 * B, M, K, 128, true)) {
+      set_error("cuTensorMapEncodeTiled failed for the A operand halves");
+      return LS_ERR_CUDA;
+    }
+    r->have_tmap_c = make_c_map(&r->tmap_c, r->c, B, M, N);
+  } else if (r->tc_ok) {
     if (y_kmaj) {
       r->yk = nullptr;
       LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
@@ -870,7 +895,8 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
     }
     r->have_tmap_c = make_c_map(&r->tmap_c, r->c, B, M, N);
   }
-  r->lim.bf16 = r->tc_ok;
+  r->lim.bf16 = r->tc_ok && r->bf16;
+  r->lim.tf32x3 = r->tc_ok && !r->bf16;
   {  // general-path view of the same buffers for candidates plan_program cannot map
     GeneralWorkload alt;
     std::string aerr;

@@ -49,6 +49,7 @@ struct TcArgs {
   unsigned long long* trace;  // optional per-CTA globaltimer stamps (8 per CTA)
   uint32_t idesc;
   uint32_t tmem_cols;
+  int lo_b;  // X3: batch index offset of the lo halves in the operand maps
 };
 
 constexpr int kTile = 128 * 64 * 2;  // A stage bytes
@@ -61,7 +62,14 @@ constexpr int kEpiDirect = 2;  // mode 0, BN <= 32: each thread stores its TMEM 
 // One instantiation per (split-K mode, epilogue, tracing): every launch runs
 // straight-line code for its own case (the all-cases kernel measured 0.5 us
 // slower per bmm launch, profiles/r02_gemm_lab.md §5).
-template <int MODE, int EPI, bool TRACE>
+//
+// X3 (fp32 workloads, 3xTF32): the operands come as [hi | lo] pairs of fp32
+// tensors (hi = the top 19 bits, lo = the exact remainder; launch_split_tf32),
+// a stage holds one 32-element k sub-tile of A_hi, A_lo, B_hi, B_lo (each
+// 128-byte rows, the bf16 stage's layout), and each 8-deep k step issues
+// lo*hi + hi*lo + hi*hi as kind::tf32 UMMAs into the fp32 accumulator: fp32
+// accuracy (the dropped lo*lo term is ~2^-22 relative) at tensor-core rate.
+template <int MODE, int EPI, bool TRACE, bool X3>
 __global__ void __launch_bounds__(128, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                const __grid_constant__ CUtensorMap tmc, TcArgs a) {
@@ -71,10 +79,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const int b_bytes = a.bn * 64 * 2;
+  const int b_bytes = a.bn * 64 * 2;            // one operand tile: BN rows of 128 bytes
+  constexpr int kHalves = X3 ? 2 : 1;           // X3: hi and lo tiles of each operand
   const uint32_t a0 = base;                     // A stages
-  const uint32_t b0 = base + a.stages * kTile;  // B stages
-  const uint32_t ring = static_cast<uint32_t>(a.stages * (kTile + b_bytes));
+  const uint32_t b0 = base + a.stages * kTile * kHalves;  // B stages
+  const uint32_t ring = static_cast<uint32_t>(a.stages * (kTile + b_bytes) * kHalves);
   const uint32_t tile_bytes = EPI == kEpiDirect ? 0u
                               : EPI == kEpiTma  ? static_cast<uint32_t>(a.bn / 32) * 16384u
                                                 : static_cast<uint32_t>(128 * a.ld * 4);
@@ -115,7 +124,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
   if (TRACE && threadIdx.x == 0) tr[1] = gtime();
 
-  const uint32_t stage_bytes = kTile + b_bytes;
+  const uint32_t stage_bytes = (kTile + b_bytes) * kHalves;
   const int tile = (batch * gridDim.y + m_blk) * gridDim.x + n_blk;
   float* ctile = a.c + batch * a.sc_b + static_cast<int64_t>(m_blk) * 128 * a.sc_m + static_cast<int64_t>(n_blk) * a.bn;
   const int c4 = a.bn / 4;
@@ -152,12 +161,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
     // ---- TMA producer ----
     int s = 0;
     uint32_t ph = 0;
-    int kc = split * a.kt * 64;
-    for (int kt = 0; kt < a.kt; ++kt, kc += 64) {
+    constexpr int kStep = X3 ? 32 : 64;  // k elements per stage (128-byte rows)
+    int kc = split * a.kt * kStep;
+    for (int kt = 0; kt < a.kt; ++kt, kc += kStep) {
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
       mbar_expect_tx(full + 8 * s, stage_bytes);
-      tma_load_3d(a0 + s * kTile, &tma, full + 8 * s, kc, m_blk * 128, batch);
-      tma_load_3d(b0 + s * b_bytes, &tmb, full + 8 * s, kc, n_blk * a.bn, batch);
+      tma_load_3d(a0 + s * kTile * kHalves, &tma, full + 8 * s, kc, m_blk * 128, batch);
+      tma_load_3d(b0 + s * b_bytes * kHalves, &tmb, full + 8 * s, kc, n_blk * a.bn, batch);
+      if constexpr (X3) {
+        tma_load_3d(a0 + s * kTile * 2 + kTile, &tma, full + 8 * s, kc, m_blk * 128, batch + a.lo_b);
+        tma_load_3d(b0 + s * b_bytes * 2 + b_bytes, &tmb, full + 8 * s, kc, n_blk * a.bn, batch + a.lo_b);
+      }
       if (++s == a.stages) {
         s = 0;
         ph ^= 1;
@@ -171,10 +185,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
       if (TRACE && kt == 0) tr[2] = gtime();
-      const uint32_t sa = a0 + s * kTile, sb = b0 + s * b_bytes;
+      const uint32_t sa = a0 + s * kTile * kHalves, sb = b0 + s * b_bytes * kHalves;
+      if constexpr (X3) {
+        const uint32_t la = sa + kTile, lb = sb + b_bytes;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_tf32(tmem, sdesc(la + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+          umma_tf32(tmem, sdesc(sa + kk * 32), sdesc(lb + kk * 32), a.idesc, 1);
+          umma_tf32(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, 1);
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+      }
       if (kt + a.stages < a.kt) umma_commit(empty + 8 * s);  // the slot is refilled
       if (++s == a.stages) {
         s = 0;
@@ -285,21 +309,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ 
 
 using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcArgs);
 
-// the instantiations: (mode, epilogue) pairs tc_geom can produce, x tracing
-template <bool TRACE>
+// the instantiations: (mode, epilogue) pairs tc_geom can produce, x tracing x operand kind
+template <bool TRACE, bool X3>
 TcKernel pick_kernel(int mode, int epi) {
   if (mode == 0) {
-    if (epi == kEpiDirect) return tc_gemm_kernel<0, kEpiDirect, TRACE>;
-    if (epi == kEpiTma) return tc_gemm_kernel<0, kEpiTma, TRACE>;
-    return tc_gemm_kernel<0, kEpiStaged, TRACE>;
+    if (epi == kEpiDirect) return tc_gemm_kernel<0, kEpiDirect, TRACE, X3>;
+    if (epi == kEpiTma) return tc_gemm_kernel<0, kEpiTma, TRACE, X3>;
+    return tc_gemm_kernel<0, kEpiStaged, TRACE, X3>;
   }
-  if (mode == 2) return epi == kEpiTma ? tc_gemm_kernel<2, kEpiTma, TRACE> : tc_gemm_kernel<2, kEpiStaged, TRACE>;
-  return tc_gemm_kernel<3, kEpiStaged, TRACE>;
+  if (mode == 2)
+    return epi == kEpiTma ? tc_gemm_kernel<2, kEpiTma, TRACE, X3> : tc_gemm_kernel<2, kEpiStaged, TRACE, X3>;
+  return tc_gemm_kernel<3, kEpiStaged, TRACE, X3>;
 }
 
-TcKernel kernel_for(const TcGeom& g, bool trace) {
+TcKernel pick_kernel(int mode, int epi, bool trace, bool x3) {
+  if (x3) return trace ? pick_kernel<true, true>(mode, epi) : pick_kernel<false, true>(mode, epi);
+  return trace ? pick_kernel<true, false>(mode, epi) : pick_kernel<false, false>(mode, epi);
+}
+
+TcKernel kernel_for(const TcGeom& g, bool trace, bool x3) {
   const int epi = g.direct ? kEpiDirect : g.tma_epi ? kEpiTma : kEpiStaged;
-  return trace ? pick_kernel<true>(g.mode, epi) : pick_kernel<false>(g.mode, epi);
+  return pick_kernel(g.mode, epi, trace, x3);
 }
 
 // the smem opt-in of every instantiation (identical static smem), once
@@ -308,13 +338,13 @@ int tc_max_dyn() {
     int m = 1 << 30;
     for (int mode : {0, 2, 3})
       for (int epi : {kEpiStaged, kEpiTma, kEpiDirect})
-        for (bool t : {false, true}) {
-          if (epi == kEpiDirect && mode != 0) continue;
-          if (mode == 3 && epi != kEpiStaged) continue;
-          const int d = opt_in_dynamic_smem(reinterpret_cast<const void*>(t ? pick_kernel<true>(mode, epi)
-                                                                             : pick_kernel<false>(mode, epi)));
-          m = std::min(m, d);
-        }
+        for (bool t : {false, true})
+          for (bool x3 : {false, true}) {
+            if (epi == kEpiDirect && mode != 0) continue;
+            if (mode == 3 && epi != kEpiStaged) continue;
+            const int d = opt_in_dynamic_smem(reinterpret_cast<const void*>(pick_kernel(mode, epi, t, x3)));
+            m = std::min(m, d);
+          }
     return m;
   }();
   return max_dyn;
@@ -327,7 +357,7 @@ void preload_tc_gemm() { tc_max_dyn(); }
 bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   const int max_dyn = tc_max_dyn();
   if (max_dyn <= 0 || L.smem_bytes > max_dyn) return false;
-  const TcGeom g = tc_geom(L.bn, L.splits, L.stages, static_cast<int64_t>(L.batch) * L.grid_m * L.grid_n);
+  const TcGeom g = tc_geom(L.bn, L.splits, L.stages, static_cast<int64_t>(L.batch) * L.grid_m * L.grid_n, L.x3);
   if (g.mode == 2 && !L.sync) return false;
   if (g.tma_epi && !L.tmap_c) return false;  // smem was planned for the TMA epilogue
   TcArgs a;
@@ -336,13 +366,16 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   a.sc_m = L.sc_m;
   a.bn = L.bn;
   a.splits = L.splits;
-  a.kt = L.kt;
+  a.kt = L.x3 ? 2 * L.kt : L.kt;  // X3: stages are 32-element k sub-tiles
+  a.lo_b = L.x3 ? L.batch : 0;
   a.stages = L.stages;
   a.ld = g.ld;
   a.sync = L.sync;
   a.trace = L.trace;
-  // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N>>3, M>>4
-  a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(L.bn >> 3) << 17) |
+  // instruction descriptor: D f32, A/B bf16 (kind::f16) or tf32 (kind::tf32),
+  // both K-major, N>>3, M>>4
+  const uint32_t fmt = L.x3 ? 2u : 1u;
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(L.bn >> 3) << 17) |
             (static_cast<uint32_t>(128 >> 4) << 24);
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(L.bn)) cols <<= 1;
@@ -361,7 +394,7 @@ bool launch_tc_gemm(const TcLaunch& L, cudaStream_t st) {
   const CUtensorMap ta = *static_cast<const CUtensorMap*>(L.tmap_a);
   const CUtensorMap tb = *static_cast<const CUtensorMap*>(L.tmap_b);
   const CUtensorMap tc = L.tmap_c ? *static_cast<const CUtensorMap*>(L.tmap_c) : tb;
-  if (cudaLaunchKernelEx(&cfg, kernel_for(g, L.trace != nullptr), ta, tb, tc, a) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&cfg, kernel_for(g, L.trace != nullptr, L.x3), ta, tb, tc, a) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }

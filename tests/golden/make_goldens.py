@@ -184,6 +184,8 @@ POPULATIONS = {
     "bert_ffn": (lambda: ls.gmm(128, 768, 3072), T.b200_space_config(), 8192),
     "bmm_qk": (lambda: W.batch_matmul(12, 128, 128, 64), T.b200_space_config(), 8192),
     "gmm512": (lambda: ls.gmm(512, 512, 512), ls.default_space_config(), 8192),
+    # config 1 with the tcgen05 module: fp32 tiles run as 3xTF32
+    "gmm512_tc": (lambda: ls.gmm(512, 512, 512), T.b200_space_config(), 8192),
     "conv2d": (lambda: W.conv2d_nhwc(), T.b200_space_config(), 8192),
     "bert_dense": (lambda: ls.gmm(128, 768, 768), T.b200_space_config(), 1024),
     "bert_ffn_in": (lambda: ls.gmm(128, 3072, 768), T.b200_space_config(), 1024),

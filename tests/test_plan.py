@@ -33,10 +33,24 @@ def test_population_families_bert_ffn():
             assert 1 <= stages <= min(kt, 8)
 
 
-def test_fp32_has_no_tensor_core_family():
+def test_fp32_tensor_core_tile_is_3xtf32():
+    # the same tcgen05 tile on an fp32 workload: 3xTF32 (cfg[8] = 1), same
+    # grid / BN / split-K / k-tiles as the bf16 instantiation; its ring slots
+    # are 32-element k sub-tiles of twice the bf16 stage bytes
     hdr, pop = load_population("bert_ffn")
-    res = plan(hdr["e0"], [p["program"] for p in pop[:300]], dtype="f32")
-    assert not any(r["family"] == "tcgen05" for r in res)
+    progs = [p["program"] for p in pop[:300]]
+    r16 = plan(hdr["e0"], progs)
+    r32 = plan(hdr["e0"], progs, dtype="f32")
+    n = 0
+    for a, b in zip(r16, r32):
+        assert (a["family"] == "tcgen05") == (b["family"] == "tcgen05")
+        if a["family"] != "tcgen05":
+            continue
+        if a["status"] == "OK" and b["status"] == "OK":
+            assert a["cfg"][:6] == b["cfg"][:6] and a["cfg"][8] == 0 and b["cfg"][8] == 1
+            assert 1 <= b["cfg"][6] <= min(2 * b["cfg"][5], 8)
+            n += 1
+    assert n > 10
 
 
 def test_simt_mapping_matches_mlt_bands():
@@ -159,3 +173,8 @@ def test_traced_pipeline_depth_sets_tcgen05_stages():
         else:
             assert r["status"] == "ILLEGAL"
     assert len(depths) >= 3
+    # fp32: the same traced depth in k-tiles is twice as many 32-element slots
+    res32 = plan(ls.ir.serialize(e0), progs, dtype="f32")
+    for p, r in zip(progs, res32):
+        if r["family"] == "tcgen05" and r["status"] == "OK":
+            assert r["cfg"][8] == 1 and r["cfg"][6] == 2 * unrolled(p)[0], (r["cfg"], unrolled(p))
