@@ -429,7 +429,7 @@ def run_b200(args):
 
     # isolated single launch of the best schedule: the checked launch alone
     # (events around one launch, L2-warm, nothing before or after it in flight)
-    isolated_us = None
+    isolated_us = isolated_kernel_us = None
     if best is not None:
         iso = B200Runner(device=local, dtype=dtype, min_repeats=1, max_repeats=1, target_ms=0.0,
                          timeout_ms=timeout_ms)
@@ -439,6 +439,14 @@ def run_b200(args):
             x, = iso.measure_programs([best_text])
             if x["status"] == "OK":
                 vals.append(x["checked_ns"] / 1e3)
+        # the same launch's device-side span (first CTA start -> last CTA
+        # end, globaltimer): events around a lone launch also include ~6-7 us
+        # of launch latency outside the kernel
+        if best["family"] in ("tcgen05", "tcgen05_conv"):
+            try:
+                isolated_kernel_us = iso.kernel_span_us(best_text)
+            except Exception:
+                isolated_kernel_us = None
         iso.close()
         isolated_us = statistics.median(vals) if vals else None
 
@@ -499,6 +507,7 @@ def run_b200(args):
                 "tflops": best_tflops, "frac_of_peak": best_tflops / peak,
                 "peak": peak, "peak_source": peak_note,
                 "latency_us": best["latency_ns"] / 1e3, "isolated_us": isolated_us,
+                "isolated_kernel_us": isolated_kernel_us,
                 "cold_l2_us": cold_us,
                 "family": best["family"], "cfg": best["cfg"],
                 "repeats": best["repeats"], "latency_us_in_step": best_in_step_us,
@@ -522,6 +531,8 @@ def run_b200(args):
                 "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
                 "traffic": traffic_bytes, "traffic_source": traffic_src,
                 "frac_isolated": None if not isolated_us else flops / (isolated_us * 1e-6) / 1e12 / peak,
+                "frac_isolated_kernel": None if not isolated_kernel_us else
+                flops / (isolated_kernel_us * 1e-6) / 1e12 / peak,
                 "frac_cold_l2": None if not cold_us else flops / (cold_us * 1e-6) / 1e12 / peak,
                 "kernel": f"best candidate ({best['family']}), L2-warm back-to-back repeats"},
             "cpu_baseline": cpu,

@@ -173,6 +173,29 @@ class B200Runner:
         native.check(native.lib().ls_runner_launch_count(self._h, ctypes.byref(v)), "launches")
         return int(v.value)
 
+    def trace_tc(self, program, launches: int = 1, max_ctas: int = 1 << 15) -> np.ndarray:
+        """Per-CTA ``%globaltimer`` stamps of a tcgen05 GEMM / conv candidate
+        (``ls_runner_trace_tc``): [launches * n_ctas, 8] int64 ns -- start,
+        setup done, first stage landed, accumulator done, partial staged,
+        zeroing flag acquired, stored, smid."""
+        b = program_text(program).encode()
+        buf = (ctypes.c_uint64 * (8 * max_ctas))()
+        n = ctypes.c_int()
+        native.check(native.lib().ls_runner_trace_tc(self._h, b, len(b), launches, buf, max_ctas,
+                                                     ctypes.byref(n)), "ls_runner_trace_tc")
+        return np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8)[: n.value * launches].astype(np.int64)
+
+    def kernel_span_us(self, program, samples: int = 5) -> float:
+        """Device-side duration of ONE isolated launch of a tcgen05 candidate:
+        first CTA start to last CTA end (globaltimer), median of ``samples``
+        single-launch traces -- the kernel without the host/driver launch
+        latency that CUDA events around a lone launch also include."""
+        spans = []
+        for _ in range(samples):
+            a = self.trace_tc(program, 1)
+            spans.append((a[:, 6].max() - a[:, 0].min()) / 1e3)
+        return float(np.median(spans))
+
     def debug_stats(self, launch_host_us: float = 0.0) -> dict:
         a = np.zeros(8, np.float64)
         a[7] = launch_host_us

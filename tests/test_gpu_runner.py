@@ -460,3 +460,26 @@ def test_baseline_relative_deadline_cap():
     y, = r.measure_programs([progs[slow[0]]])
     assert y["status"] == "OK" and y["mismatches"] == 0, y
     r.close()
+
+
+def test_trace_tc_kernel_span():
+    # per-CTA globaltimer stamps of one isolated tcgen05 launch: every CTA
+    # stamped in order, the kernel's device span well under the events'
+    # launch-to-launch time and the output still exact
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    r = make_runner("bf16")
+    r.set_workload(e0, seed=0)
+    plans = r.plan_programs(progs)
+    i = next(i for i, p in enumerate(plans) if p["family"] == "tcgen05" and p["status"] == "OK"
+             and p["cfg"][4] > 1)
+    a = r.trace_tc(progs[i], 1)
+    b, gm, gn, bn, splits = plans[i]["cfg"][:5]
+    assert a.shape == (b * gm * gn * splits, 8)
+    assert (a[:, 0] > 0).all() and (np.diff(a[:, [0, 1, 2, 3, 4, 6]], axis=1) >= 0).all()
+    span = r.kernel_span_us(progs[i], samples=3)
+    assert 0.5 < span < 200.0, span
+    res, = r.measure_programs([progs[i]])
+    assert res["status"] == "OK" and res["mismatches"] == 0
+    r.close()
