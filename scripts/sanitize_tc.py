@@ -3,7 +3,8 @@ kernel instantiation the population reaches -- split-K mode (0: no split; 2:
 arrival ticket + in-kernel zeroing + add-reduce) x epilogue (register-direct
 for unsplit BN <= 32, TMA store / add-reduce for BN % 32 == 0, staged
 otherwise) -- each measured a few times through the Runner (checked launch +
-timed repeats), outputs compared with the fp64 reference run.  Run as
+timed repeats), outputs compared with the fp64 reference run.  The fp32
+workloads cover the 3xTF32 instantiations of the same modes.  Run as
   compute-sanitizer --tool {memcheck,racecheck,synccheck} python scripts/sanitize_tc.py
 """
 import gzip
@@ -26,10 +27,13 @@ def load(name):
 
 def main():
     bad = 0
-    for name, fam, cfg_split, cfg_bn in (("bert_ffn", "tcgen05", 4, 3), ("bmm_qk", "tcgen05", 4, 3),
-                                         ("conv2d", "tcgen05_conv", 3, 2)):
+    for name, fam, cfg_split, cfg_bn, dtype in (("bert_ffn", "tcgen05", 4, 3, "bf16"),
+                                                ("bmm_qk", "tcgen05", 4, 3, "bf16"),
+                                                ("conv2d", "tcgen05_conv", 3, 2, "bf16"),
+                                                ("gmm512_tc", "tcgen05", 4, 3, "f32"),
+                                                ("bmm_qk", "tcgen05", 4, 3, "f32")):
         e0, progs = load(name)
-        r = B200Runner(device=0, dtype="bf16", min_repeats=2, max_repeats=2, target_ms=0.001, timeout_ms=60000.0)
+        r = B200Runner(device=0, dtype=dtype, min_repeats=2, max_repeats=2, target_ms=0.001, timeout_ms=60000.0)
         r.set_workload(e0, seed=0)
         want = r.reference_output()
         plans = r.plan_programs(progs)
@@ -48,7 +52,7 @@ def main():
             out = r.last_output().astype(np.float64)
             ok = res["status"] == "OK" and res["mismatches"] == 0 and np.array_equal(out, want)
             bad += not ok
-            print(f"{name} {fam} {mode} cfg={res['cfg']} status={res['status']} mismatches={res['mismatches']} "
+            print(f"{name} {dtype} {fam} {mode} cfg={res['cfg']} status={res['status']} mismatches={res['mismatches']} "
                   f"exact={ok}", flush=True)
         r.close()
     print("SANITIZE_DRIVER_DONE bad=%d" % bad)
