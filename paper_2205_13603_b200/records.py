@@ -115,7 +115,10 @@ def report_json(report, ctx: HardwareContext, info: Optional[dict] = None, times
         t = ctx.tflops(report.best.latency)
         hw["best"] = {"tflops": t, "latency_unit": ctx.unit, **info.get(report.best.program_hash, {})}
         if t is not None and ctx.peak_tflops:
-            hw["best"]["roofline"] = {"bound": "tensor", "peak": ctx.peak_tflops, "unit": "TFLOP/s",
+            fam = hw["best"].get("family")
+            bound = ("fp32-simt" if fam not in (None, "tcgen05", "tcgen05_conv") and ctx.dtype != "bf16"
+                     else "tensor")
+            hw["best"]["roofline"] = {"bound": bound, "peak": ctx.peak_tflops, "unit": "TFLOP/s",
                                       "frac": t / ctx.peak_tflops, "peak_source": ctx.peak_source}
     doc["hardware"] = hw
     return doc

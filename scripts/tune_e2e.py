@@ -2,6 +2,7 @@
 (plugin.py), BASELINE configs 1 and 5:
 
   python scripts/tune_e2e.py gmm512      # config 1: gmm 512^3 fp32, 64 trials, seed 0
+  python scripts/tune_e2e.py gmm512_tc   # config 1 with the tcgen05 module (fp32 tiles as 3xTF32)
   python scripts/tune_e2e.py bert [N]    # config 5: BERT-base tasks, N trials (default 2000)
 
 Needs the reference package importable (baseline/_ref).  Prints one JSON
@@ -25,20 +26,25 @@ def peak():
         return None
 
 
-def gmm512():
+def gmm512(tc=False):
     ls = loopsched()
     e0 = ls.gmm(512, 512, 512)
+    if tc:
+        from paper_2205_13603_b200.tensor_core import b200_space
+    space = b200_space if tc else ls.default_space
     cfg = ls.SearchConfig(trials=64, batch=16, population=64, seed=0)
     t0 = time.perf_counter()
-    rep_p = plugin.tune(e0, ls.default_space(), cfg, mode="parity")
+    rep_p = plugin.tune(e0, space(), cfg, mode="parity")
     t_par = time.perf_counter() - t0
     t0 = time.perf_counter()
-    rep, doc = plugin.tune_with_records(e0, ls.default_space(), cfg, mode="hardware", dtype="f32",
-                                        peak_tflops=148 * 128 * 2 * 1.965e9 / 1e12,
-                                        peak_source="fp32 SIMT nominal", timeout_ms=5.0, timeout_factor=10.0,
+    bf16 = peak()
+    rep, doc = plugin.tune_with_records(e0, space(), cfg, mode="hardware", dtype="f32",
+                                        peak_tflops=bf16 / 6 if tc and bf16 else 148 * 128 * 2 * 1.965e9 / 1e12,
+                                        peak_source="3xTF32 roof (measured bf16 / 6)" if tc and bf16
+                                        else "fp32 SIMT nominal", timeout_ms=5.0, timeout_factor=10.0,
                                         min_repeats=3, max_repeats=50, target_ms=0.05)
     t_hw = time.perf_counter() - t0
-    return {"config": "gmm512 fp32, default space, 64 trials, seed 0",
+    return {"config": "gmm512 fp32, %s, 64 trials, seed 0" % ("default space + use_tensor_core" if tc else "default space"),
             "parity_mode": {"best_cycles": str(rep_p.best.latency), "wall_s": t_par, "trials": len(rep_p.log)},
             "hardware_mode": {"wall_s": t_hw, "trials": len(rep.log), "best_ns": float(rep.best.latency),
                               "baseline_ns": float(rep.baseline_latency), "speedup": rep.speedup,
@@ -74,5 +80,8 @@ def bert(total):
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "gmm512"
-    out = gmm512() if what == "gmm512" else bert(int(sys.argv[2]) if len(sys.argv) > 2 else 2000)
+    if what.startswith("gmm512"):
+        out = gmm512(tc=what == "gmm512_tc")
+    else:
+        out = bert(int(sys.argv[2]) if len(sys.argv) > 2 else 2000)
     print(json.dumps(out, default=str))
