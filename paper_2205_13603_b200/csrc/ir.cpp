@@ -341,8 +341,6 @@ int Program::buffer_id(std::string_view name) const {
 
 std::unique_ptr<Program> parse_program(std::string_view text, std::string* err) {
   auto p = std::make_unique<Program>();
-  p->expr_pool.reserve(text.size() / 16 + 16);  // ~one node per 20-40 bytes of JSON
-  p->stmt_pool.reserve(text.size() / 128 + 8);
   Reader r(text, p.get());
   if (!r.parse_top() || !r.good()) {
     if (err) *err = r.error().empty() ? "parse error" : r.error();

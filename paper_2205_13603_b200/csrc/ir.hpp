@@ -61,17 +61,32 @@ struct IntrinsicInfo {
 };
 const IntrinsicInfo* intrinsic_registry(int* n);
 
+// Node storage: fixed-size chunks, so a parse costs one allocation per chunk
+// instead of one per node (nodes never move; freed with the program).
+template <class T, size_t kChunk>
+struct NodeArena {
+  std::vector<std::unique_ptr<T[]>> chunks;
+  size_t used = kChunk;
+  T* alloc() {
+    if (used == kChunk) {
+      chunks.emplace_back(new T[kChunk]);
+      used = 0;
+    }
+    return &chunks.back()[used++];
+  }
+};
+
 struct Program {
   std::vector<Buffer> buffers;
   std::vector<std::string> vars;  // var id -> name
   std::vector<Stmt*> root;
   // ownership
-  std::vector<std::unique_ptr<Expr>> expr_pool;
-  std::vector<std::unique_ptr<Stmt>> stmt_pool;
+  NodeArena<Expr, 64> expr_pool;
+  NodeArena<Stmt, 16> stmt_pool;
 
   int buffer_id(std::string_view name) const;
-  Expr* new_expr() { expr_pool.emplace_back(new Expr()); return expr_pool.back().get(); }
-  Stmt* new_stmt() { stmt_pool.emplace_back(new Stmt()); return stmt_pool.back().get(); }
+  Expr* new_expr() { return expr_pool.alloc(); }
+  Stmt* new_stmt() { return stmt_pool.alloc(); }
 };
 
 // Parses `text`; on failure returns nullptr and fills `err`.
