@@ -68,6 +68,20 @@ def contraction_flops(e0_json: str) -> float:
     return 2.0 * walk(json.loads(e0_json)["root"])
 
 
+def algorithmic_bytes(e0_json: str, dtype: str) -> int:
+    """every input read once (runner dtype) + every output
+    written once (fp32)."""
+    import math
+    tot = 0
+    for b in json.loads(e0_json)["buffers"]:
+        n = math.prod(b["shape"])
+        if b["role"] == "input":
+            tot += n * (2 if dtype == "bf16" else 4)
+        elif b["role"] == "output":
+            tot += n * 4
+    return tot
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -399,6 +413,8 @@ def run_b200(args):
     x3 = dtype != "bf16" and best is not None and best["family"] == "tcgen05"
     peak = peak_bf16 if dtype == "bf16" else peak_bf16 / 6 if x3 else fp32_peak
     bound = "tensor" if dtype == "bf16" else "tensor (3xTF32)" if x3 else "fp32-simt"
+    algo_bytes = algorithmic_bytes(e0, dtype)
+    attainable = min(peak, flops / algo_bytes * peak_hbm / 1e3)
     peak_note = (peak_src if dtype == "bf16" else
                  f"{peak_src} bf16 / 6 (tf32 = bf16 / 2, three passes)" if x3 else "fp32 SIMT nominal")
     best_tflops = flops / (best["latency_ns"] * 1e-9) / 1e12 if best else None
@@ -530,6 +546,9 @@ def run_b200(args):
                 "frac_of_fp32_simt_peak": None if dtype == "bf16" else best_tflops / fp32_peak,
                 "peak": peak, "unit": "TFLOP/s", "frac": best_tflops / peak,
                 "traffic": traffic_bytes, "traffic_source": traffic_src,
+                "algorithmic_bytes": algo_bytes, "arithmetic_intensity": flops / algo_bytes,
+                "attainable": attainable, "frac_attainable": best_tflops / attainable,
+                "attainable_what": "SURVEY §8(d): min(peak, arithmetic intensity x measured HBM GB/s)",
                 "frac_isolated": None if not isolated_us else flops / (isolated_us * 1e-6) / 1e12 / peak,
                 "frac_isolated_kernel": None if not isolated_kernel_us else
                 flops / (isolated_kernel_us * 1e-6) / 1e12 / peak,
