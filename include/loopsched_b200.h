@@ -91,7 +91,8 @@ void ls_batch_destroy(ls_batch* b);
 typedef enum { LS_DTYPE_F32 = 0, LS_DTYPE_BF16 = 1 } ls_dtype;
 
 typedef struct {
-  int32_t dtype;           /* ls_dtype of the device copies of the inputs          */
+  int32_t dtype;           /* ls_dtype of the device copies of the inputs; with    */
+                           /* LS_DTYPE_F32 a tcgen05 tile runs as 3xTF32           */
   int32_t min_repeats;     /* timed launches per candidate (lower bound)          */
   int32_t max_repeats;     /* upper bound                                          */
   double target_ms;        /* repeats sized so one candidate runs ~target_ms       */

@@ -27,6 +27,9 @@
 //     memsets before the launch.
 // Instantiated at runtime for any BN in [16, 256] step 16, split-K ways,
 // k-tiles and stage count (see plan.cpp).
+//
+// fp32 workloads (X3): the same tile as 3xTF32 -- see the X3 note at the
+// kernel template; cfg[8] = 1 in the planner's report.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
