@@ -261,12 +261,17 @@ bool tc_conv_plan(const GeneralWorkload& w, const Program& p, const Stmt* s, con
   }
   if (t.c0 % 4 || t.cc_h1 % 4 || t.cc_w1 % 4) return false;
   if (t.splits * t.kt > kConvMaxK) return false;  // per-k-tile coordinate table (tc_conv.cu)
-  const int64_t stage = 128 * 64 * 2 + t.bn * 64 * 2;
-  const bool cluster = t.splits > 1;
+  // fp32 (3xTF32): a ring slot is one 32-channel k sub-tile, hi and lo halves
+  // of both operands (twice the bf16 slot), two slots per k-tile; its split-K
+  // uses the L2 tickets only (no cluster)
+  t.x3 = !lim.bf16;
+  const int64_t per_kt = t.x3 ? 2 : 1;
+  const int64_t stage = (128 * 64 * 2 + t.bn * 64 * 2) * per_kt;
+  const bool cluster = t.splits > 1 && !t.x3;
   const int64_t rows_per = (64 + t.splits - 1) / t.splits;
   const int64_t red = cluster ? t.splits * rows_per * (t.bn + 4) * 4 : 64 * (t.bn + 4) * 4;
   int64_t avail = lim.max_smem - 2048 - (cluster ? red : 0);
-  t.stages = std::min<int64_t>(t.kt, std::max<int64_t>(1, avail / stage));
+  t.stages = std::min<int64_t>(per_kt * t.kt, std::max<int64_t>(1, avail / stage));
   t.stages = std::min<int64_t>(t.stages, 8);
   t.smem_bytes = (cluster ? t.stages * stage + red : std::max(t.stages * stage, red)) + 1024 + 256;
   return true;
@@ -643,7 +648,10 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
       }
     }
     // ---- TCGEN05 conv: innermost [p 8][q 8][co BN][ci 64] (bf16) ----
-    if (lim.bf16 && tc_conv_plan(w, p, s, xl, yl, lps, cond != nullptr, lim, &step.conv)) {
+    // fp32: the 3xTF32 tile reads operand halves the runner splits once, so
+    // its activation must be a workload input (not an in-candidate pad stage)
+    const bool x3_ok = lim.tf32x3 && p.buffers[static_cast<size_t>(xl->buffer)].role == 0;
+    if ((lim.bf16 || x3_ok) && tc_conv_plan(w, p, s, xl, yl, lps, cond != nullptr, lim, &step.conv)) {
       step.family = F_TCCONV;
       step.x_buf = xl->buffer;
       step.y_buf = yl->buffer;
@@ -655,6 +663,7 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
       o[2] = static_cast<int32_t>(t.bn); o[3] = static_cast<int32_t>(t.splits);
       o[4] = static_cast<int32_t>(t.kt); o[5] = static_cast<int32_t>(t.stages);
       o[6] = static_cast<int32_t>(t.smem_bytes / 1024);
+      o[7] = t.x3 ? 1 : 0;
       plan.steps.push_back(step);
       if (t.bn > 256 || t.splits > 16) { plan.status = P_ILLEGAL; plan.why = "conv tile beyond tcgen05 limits"; return plan; }
       if (t.smem_bytes > lim.max_smem) { plan.status = P_ILLEGAL; plan.why = "smem above limit"; return plan; }

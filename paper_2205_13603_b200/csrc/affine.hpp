@@ -78,6 +78,7 @@ struct TcConvCfg {
   int64_t c0;                      // output address constant
   int64_t cc_h1, cc_w1;            // output address per box row / box column
   int64_t bn, splits, kt, stages, smem_bytes, grid_m, grid_n;
+  bool x3;  // fp32 operands as 3xTF32 halves; stages are then 32-channel k sub-tiles (two per k-tile)
 };
 
 // Buffer ids of the candidate program, resolved by name against the runner's

@@ -108,18 +108,22 @@ bool make_nhwc_out_map(CUtensorMap* map, void* base, const int64_t* shape) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// bf16 NHWC activation [n][h][w][c] as a 4-D TMA map with an {64, 8, 8, 1}
-// box (one 8 x 8 pixel box x 64 channels); out-of-bounds boxes read zeros.
-bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape) {
+// NHWC activation [n][h][w][c] as a 4-D TMA map whose box is one 8 x 8 pixel
+// box of 128-byte channel rows: {64, 8, 8, 1} of bf16, or {32, 8, 8, 1} of
+// fp32 over the [hi | lo] halves of the 3xTF32 tile (n doubled, lo at n + N);
+// out-of-bounds boxes read zeros.
+bool make_nhwc_map(CUtensorMap* map, void* base, const int64_t* shape, bool f32 = false) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
+  const int64_t es = f32 ? 4 : 2;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(shape[3]), static_cast<cuuint64_t>(shape[2]),
-                        static_cast<cuuint64_t>(shape[1]), static_cast<cuuint64_t>(shape[0])};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(shape[3] * 2), static_cast<cuuint64_t>(shape[2] * shape[3] * 2),
-                           static_cast<cuuint64_t>(shape[1] * shape[2] * shape[3] * 2)};
-  cuuint32_t box[4] = {64, 8, 8, 1};
+                        static_cast<cuuint64_t>(shape[1]), static_cast<cuuint64_t>(shape[0] * (f32 ? 2 : 1))};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(shape[3] * es), static_cast<cuuint64_t>(shape[2] * shape[3] * es),
+                           static_cast<cuuint64_t>(shape[1] * shape[2] * shape[3] * es)};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / es), 8, 8, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -220,6 +224,8 @@ struct ls_runner {
     has_alt = false;
     pfree(wt);
     wt = nullptr;
+    for (void* h : gbuf_x3) pfree(h);
+    gbuf_x3.clear();
     tmap_wt.clear();
     tmap_x.clear();
     tmap_o.clear();
@@ -339,8 +345,9 @@ struct ls_runner {
   int64_t* gcode = nullptr;     // concatenated bytecode of the current batch
   size_t gcode_cap = 0;
   // tcgen05 conv: K-major weight copy [n_cols][k_rows] and tensor-map caches
-  void* wt = nullptr;
+  void* wt = nullptr;            // bf16; fp32 workloads: [hi | lo] halves (3xTF32)
   int64_t wt_rows = 0, wt_cols = 0;
+  std::vector<void*> gbuf_x3;    // fp32 workloads: [hi | lo] halves of each NHWC input (or null)
   std::map<int, CUtensorMap> tmap_wt;         // by BN
   std::map<const void*, CUtensorMap> tmap_x;  // by activation buffer
 
@@ -349,7 +356,7 @@ struct ls_runner {
     auto it = tmap_wt.find(bn);
     if (it != tmap_wt.end()) return &it->second;
     CUtensorMap m;
-    if (!wt || !make_kmajor_map(&m, wt, 1, wt_cols, wt_rows, bn)) return nullptr;
+    if (!wt || !make_kmajor_map(&m, wt, bf16 ? 1 : 2, wt_cols, wt_rows, bn, !bf16)) return nullptr;
     return &(tmap_wt[bn] = m);
   }
   std::map<const void*, CUtensorMap> tmap_o;  // fp32 NHWC conv outputs, box {32, 8, 8, 1}
@@ -366,7 +373,7 @@ struct ls_runner {
     auto it = tmap_x.find(buf);
     if (it != tmap_x.end()) return &it->second;
     CUtensorMap m;
-    if (!make_nhwc_map(&m, const_cast<void*>(buf), shape)) return nullptr;
+    if (!make_nhwc_map(&m, const_cast<void*>(buf), shape, !bf16)) return nullptr;
     return &(tmap_x[buf] = m);
   }
 
@@ -392,8 +399,15 @@ struct ls_runner {
       GenBlock g = p.gp->gen.blocks[static_cast<size_t>(stp.block)];
       bool ok = true;
       if (stp.family == F_TCCONV) {
-        if (B.dtype[stp.x_buf] != 0 || p.gp->gen.ndim[stp.x_buf] != 4) return false;
-        const CUtensorMap* mx = map_x(B.ptr[stp.x_buf], B.shape[stp.x_buf]);
+        if (p.gp->gen.ndim[stp.x_buf] != 4 || B.dtype[stp.x_buf] != (stp.conv.x3 ? 1 : 0)) return false;
+        const void* xsrc = B.ptr[stp.x_buf];
+        if (stp.conv.x3) {  // the activation's [hi | lo] halves (a workload input, split at set_workload)
+          auto it = std::find(gw.buffers.begin(), gw.buffers.end(), p.gp->buf_names[static_cast<size_t>(stp.x_buf)]);
+          const size_t gi = static_cast<size_t>(it - gw.buffers.begin());
+          if (it == gw.buffers.end() || gi >= gbuf_x3.size() || !gbuf_x3[gi]) return false;
+          xsrc = gbuf_x3[gi];
+        }
+        const CUtensorMap* mx = map_x(xsrc, B.shape[stp.x_buf]);
         const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
         if (!mx || !mw) return false;
         uint32_t* sy = slot >= 0 && static_cast<size_t>(slot) < sync_off.size() && sync_off[static_cast<size_t>(slot)] >= 0
@@ -403,7 +417,7 @@ struct ls_runner {
                                     ? map_o(B.ptr[stp.c_buf], B.shape[stp.c_buf])
                                     : nullptr;
         ok = launch_tc_conv(mx, mw, static_cast<float*>(B.ptr[stp.c_buf]), stp.conv, true, q, trace, sy, mc,
-                            mc ? B.shape[stp.c_buf] : nullptr);
+                            mc ? B.shape[stp.c_buf] : nullptr, static_cast<int>(B.shape[stp.x_buf][0]));
       } else if (stp.family == F_AFFCOPY) {
         ok = launch_affcopy(stp.copy, B, dl, flag, q);
       } else if (stp.family == F_SIMTA) {
@@ -631,7 +645,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
   r->tc_ok = false;
   r->lim.bf16 = false;
   r->lim.tf32x3 = false;
-  for (size_t b = 0; b < nb && r->bf16; ++b) {
+  for (size_t b = 0; b < nb; ++b) {
     if (gw.buffers[b] != gw.y_buf || gw.roles[b] != 0) continue;
     const std::vector<int64_t>& sh = gw.shapes[b];
     int64_t elems = 1;
@@ -639,11 +653,30 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     r->wt_cols = sh.back();
     r->wt_rows = elems / r->wt_cols;
     if (r->wt_rows % 64 || r->wt_cols % 16) break;
-    LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 2));
-    launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
-                          r->wt_rows, r->wt_cols, r->st);
-    LSB_CUDA(cudaGetLastError());
-    r->lim.bf16 = true;
+    if (r->bf16) {
+      LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 2));
+      launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
+                            r->wt_rows, r->wt_cols, r->st);
+      LSB_CUDA(cudaGetLastError());
+      r->lim.bf16 = true;
+    } else {
+      // 3xTF32 conv tile: weight halves K-major, and halves of every NHWC
+      // input whose channels fill whole 32-element (128-byte) rows
+      LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 8));
+      launch_split_tf32(static_cast<const float*>(r->gbuf[b]), static_cast<float*>(r->wt), 1, r->wt_rows, r->wt_cols,
+                        true, r->st);
+      r->gbuf_x3.assign(nb, nullptr);
+      for (size_t x = 0; x < nb; ++x) {
+        if (gw.roles[x] != 0 || gw.shapes[x].size() != 4 || gw.shapes[x][3] % 32) continue;
+        int64_t xe = 1;
+        for (int64_t v : gw.shapes[x]) xe *= v;
+        LSB_CUDA(r->pmalloc(&r->gbuf_x3[x], static_cast<size_t>(xe) * 8));
+        launch_split_tf32(static_cast<const float*>(r->gbuf[x]), static_cast<float*>(r->gbuf_x3[x]), 1,
+                          xe / gw.shapes[x][3], gw.shapes[x][3], false, r->st);
+      }
+      LSB_CUDA(cudaGetLastError());
+      r->lim.tf32x3 = true;
+    }
   }
   r->have_workload = true;
   r->best_valid = false;
@@ -680,12 +713,13 @@ ls_status ls_plan_programs(const char* e0, size_t e0_len, const char* const* pro
   DeviceLimits lim;
   lim.bf16 = !general && dtype == LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
   lim.tf32x3 = !general && dtype != LS_DTYPE_BF16 && w.x_kmajor && w.sc[R_N] == 1;
-  if (general && dtype == LS_DTYPE_BF16)
+  if (general)
     for (size_t b = 0; b < gw.buffers.size(); ++b)
       if (gw.buffers[b] == gw.y_buf && gw.roles[b] == 0) {
         int64_t elems = 1;
         for (int64_t x : gw.shapes[b]) elems *= x;
-        lim.bf16 = (elems / gw.shapes[b].back()) % 64 == 0 && gw.shapes[b].back() % 16 == 0;
+        const bool ok = (elems / gw.shapes[b].back()) % 64 == 0 && gw.shapes[b].back() % 16 == 0;
+        (dtype == LS_DTYPE_BF16 ? lim.bf16 : lim.tf32x3) = ok;
       }
   std::vector<Plan> plans;
   GeneralWorkload alt;

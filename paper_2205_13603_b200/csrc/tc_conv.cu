@@ -62,6 +62,7 @@ struct TcConvArgs {
   int pair;                   // two boxes per CTA (grid y = pairs of boxes)
   int grid_m;                 // boxes (pair: the odd last pair has one)
   int64_t oshape[4];          // output [n][p][q][k] (decodes the box origin for the C tensor map)
+  int lo_n;                   // X3: image offset of the lo halves in the X map
 };
 
 struct Coord {
@@ -99,12 +100,18 @@ void host_add_parts(const CList& L, int64_t idx, Coord& a) {
   }
 }
 
-// one instantiation per (split-K mode, epilogue, tracing), as tc_gemm.cu
-template <int MODE, bool TMA_EPI, bool TRACE>
+// one instantiation per (split-K mode, epilogue, tracing, operand kind), as
+// tc_gemm.cu.  X3 (fp32 workloads, 3xTF32): a ring slot holds one 32-channel
+// k sub-tile -- A_hi, A_lo, B_hi, B_lo, each in the bf16 slot's 128-byte-row
+// layout -- two slots per (tap, 64 channels) k-tile, and each 8-deep k step
+// issues lo*hi + hi*lo + hi*hi as kind::tf32 UMMAs (tc_gemm.cu X3).
+template <int MODE, bool TMA_EPI, bool TRACE, bool X3>
 __global__ void __launch_bounds__(128, 1)
 tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                const __grid_constant__ CUtensorMap tmc, const __grid_constant__ TcConvArgs a) {
   static_assert(!(TMA_EPI && MODE == 1), "the cluster reduction stores from registers");
+  static_assert(!(X3 && MODE == 1), "3xTF32: L2 split-K only");
+  constexpr int kH = X3 ? 2 : 1;  // operand halves per slot
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint32_t s_ticket;
   const uint32_t raw = smem_u32(smem_raw);
@@ -112,9 +119,9 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
   uint8_t* gbase = smem_raw + (base - raw);
   const int b_bytes = a.bn * 64 * 2;
   const uint32_t a0 = base;
-  const uint32_t b0 = base + a.stages * kStageA;
+  const uint32_t b0 = base + a.stages * kStageA * kH;
   const int red_ld = a.bn + 4;
-  const uint32_t stage_end = b0 + a.stages * b_bytes;
+  const uint32_t stage_end = b0 + a.stages * b_bytes * kH;
   const int S_cl = MODE == 1 ? a.splits : 1;
   const int rows_per = (kRows + S_cl - 1) / S_cl;
   const uint32_t red = MODE == 1 ? ((stage_end + 15u) & ~15u) : base;
@@ -212,15 +219,29 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    const uint32_t stage_bytes = nbox * kLiveA + b_bytes;
+    const uint32_t stage_bytes = (nbox * kLiveA + b_bytes) * kH;
     int s = 0;
     uint32_t ph = 0;
-    for (int kt = 0; kt < a.kt; ++kt) {
+    for (int kt = 0; kt < a.kt * kH; ++kt) {
       if (kt >= a.stages) mbar_wait(empty + 8 * s, ph ^ 1);
-      const KCoord k = kc[kt];
+      const KCoord k = kc[X3 ? kt >> 1 : kt];
+      const int sub = X3 ? 32 * (kt & 1) : 0;  // X3: channel offset of the 32-wide sub-tile
       mbar_expect_tx(full + 8 * s, stage_bytes);
-      tma_load_4d(a0 + s * kStageA, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c, static_cast<int>(o.w) + k.w,
-                  static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n);
+      tma_load_4d(a0 + s * kStageA * kH, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c + sub,
+                  static_cast<int>(o.w) + k.w, static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n);
+      if constexpr (X3) {
+        tma_load_4d(a0 + s * kStageA * 2 + kStageA, &tmx, full + 8 * s, static_cast<int>(o.c) + k.c + sub,
+                    static_cast<int>(o.w) + k.w, static_cast<int>(o.h) + k.h, static_cast<int>(o.n) + k.n + a.lo_n);
+        tma_load_3d(b0 + s * b_bytes * 2, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf + sub,
+                    static_cast<int>(o.co), 0);
+        tma_load_3d(b0 + s * b_bytes * 2 + b_bytes, &tmw, full + 8 * s, static_cast<int>(o.kf) + k.kf + sub,
+                    static_cast<int>(o.co), 1);
+        if (++s == a.stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        continue;
+      }
       if (nbox == 2)  // rows 64..127: the second box (8 KB = 8 swizzle atoms in)
         tma_load_4d(a0 + s * kStageA + kLiveA, &tmx, full + 8 * s, static_cast<int>(o1.c) + k.c,
                     static_cast<int>(o1.w) + k.w, static_cast<int>(o1.h) + k.h, static_cast<int>(o1.n) + k.n);
@@ -234,14 +255,24 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
     // ---- MMA issuer (single thread) ----
     int s = 0;
     uint32_t ph = 0;
-    for (int kt = 0; kt < a.kt; ++kt) {
+    for (int kt = 0; kt < a.kt * kH; ++kt) {
       mbar_wait(full + 8 * s, ph);
       tc_fence_after();
       if (TRACE && kt == 0) tr[2] = gtime();
-      const uint32_t sa = a0 + s * kStageA, sb = b0 + s * b_bytes;
+      const uint32_t sa = a0 + s * kStageA * kH, sb = b0 + s * b_bytes * kH;
+      if constexpr (X3) {
+        const uint32_t la = sa + kStageA, lb = sb + b_bytes;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_tf32(tmem, sdesc(la + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+          umma_tf32(tmem, sdesc(sa + kk * 32), sdesc(lb + kk * 32), a.idesc, 1);
+          umma_tf32(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, 1);
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16(tmem, sdesc(sa + kk * 32), sdesc(sb + kk * 32), a.idesc, (kt | kk) != 0);
+      }
       umma_commit(empty + 8 * s);
       if (++s == a.stages) {
         s = 0;
@@ -379,11 +410,20 @@ tc_conv_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ 
 
 using ConvKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcConvArgs);
 
-template <bool TRACE>
-ConvKernel pick_conv(int mode, bool tma_epi) {
-  if (mode == 1) return tc_conv_kernel<1, false, TRACE>;
-  if (mode == 2) return tma_epi ? tc_conv_kernel<2, true, TRACE> : tc_conv_kernel<2, false, TRACE>;
-  return tma_epi ? tc_conv_kernel<0, true, TRACE> : tc_conv_kernel<0, false, TRACE>;
+template <bool TRACE, bool X3>
+ConvKernel pick_conv_t(int mode, bool tma_epi) {
+  if constexpr (!X3) {
+    if (mode == 1) return tc_conv_kernel<1, false, TRACE, false>;
+  } else {
+    if (mode == 1) return nullptr;
+  }
+  if (mode == 2) return tma_epi ? tc_conv_kernel<2, true, TRACE, X3> : tc_conv_kernel<2, false, TRACE, X3>;
+  return tma_epi ? tc_conv_kernel<0, true, TRACE, X3> : tc_conv_kernel<0, false, TRACE, X3>;
+}
+
+ConvKernel pick_conv(int mode, bool tma_epi, bool trace, bool x3) {
+  if (x3) return trace ? pick_conv_t<true, true>(mode, tma_epi) : pick_conv_t<false, true>(mode, tma_epi);
+  return trace ? pick_conv_t<true, false>(mode, tma_epi) : pick_conv_t<false, false>(mode, tma_epi);
 }
 
 // smem opt-in (and the non-portable cluster size of the mode-1 kernels) of
@@ -393,15 +433,16 @@ int conv_max_dyn() {
     int m = 1 << 30;
     for (int mode : {0, 1, 2})
       for (bool epi : {false, true})
-        for (bool t : {false, true}) {
-          if (mode == 1 && epi) continue;
-          const void* fn = reinterpret_cast<const void*>(t ? pick_conv<true>(mode, epi) : pick_conv<false>(mode, epi));
-          m = std::min(m, opt_in_dynamic_smem(fn));
-          if (mode == 1 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-            cudaGetLastError();
-            m = -1;
+        for (bool t : {false, true})
+          for (bool x3 : {false, true}) {
+            if (mode == 1 && (epi || x3)) continue;
+            const void* fn = reinterpret_cast<const void*>(pick_conv(mode, epi, t, x3));
+            m = std::min(m, opt_in_dynamic_smem(fn));
+            if (mode == 1 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+              cudaGetLastError();
+              m = -1;
+            }
           }
-        }
     return m;
   }();
   return max_dyn;
@@ -413,7 +454,7 @@ void preload_tc_conv() { conv_max_dyn(); }
 
 bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcConvCfg& g, bool pdl,
                     cudaStream_t st, unsigned long long* trace, uint32_t* sync, const void* tmap_c,
-                    const int64_t* oshape) {
+                    const int64_t* oshape, int x_images) {
   const int max_dyn = conv_max_dyn();
   if (max_dyn <= 0 || g.smem_bytes > max_dyn) return false;
   if (g.splits > kMaxClusterSplits || g.grid_m > 65535 || g.grid_n > 65535) return false;
@@ -445,6 +486,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   // split-K: L2 reduction with arrival tickets (mode 2) when the runner gave
   // ticket slots; the cluster DSMEM reduction (mode 1) otherwise
   a.mode = g.splits == 1 ? 0 : (sync && g.grid_m * g.grid_n <= kTcSyncSlots ? 2 : 1);
+  if (g.x3 && (a.mode == 1 || x_images <= 0)) return false;  // 3xTF32: L2 split-K only
+  a.lo_n = g.x3 ? x_images : 0;
   a.sync = sync;
   // TMA epilogue: the 64 box rows are the 8 x 8 pixels of an NHWC output
   // ([n][p][q][k], row r -> (p0 + r/8, q0 + r%8)) and BN is whole 32-ch chunks
@@ -454,7 +497,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     a.tma_epi = 1;
     for (int d = 0; d < 4; ++d) a.oshape[d] = oshape[d];
   }
-  a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(g.bn >> 3) << 17) |
+  const uint32_t fmt = g.x3 ? 2u : 1u;  // tf32 : bf16 operands
+  a.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(g.bn >> 3) << 17) |
             (static_cast<uint32_t>(128 >> 4) << 24);
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(g.bn)) cols <<= 1;
@@ -471,7 +515,7 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
     // than two CTAs per SM; for BN >= 32 at <= 2 CTAs per SM the extra CTAs
     // hide more latency than the dead half-rows cost
     const int64_t ctas = g.grid_m * g.grid_n * g.splits;
-    a.pair = a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && (g.bn <= 16 || ctas > 2 * 148) ? 1 : 0;
+    a.pair = !g.x3 && a.mode != 1 && g.grid_m > 1 && need <= g.smem_bytes && (g.bn <= 16 || ctas > 2 * 148) ? 1 : 0;
   }
   const int64_t grid_y = a.pair ? (g.grid_m + 1) / 2 : g.grid_m;
   cudaLaunchConfig_t cfg = {};
@@ -491,7 +535,8 @@ bool launch_tc_conv(const void* tmap_x, const void* tmap_w, float* c, const TcCo
   const CUtensorMap tx = *static_cast<const CUtensorMap*>(tmap_x);
   const CUtensorMap tw = *static_cast<const CUtensorMap*>(tmap_w);
   const CUtensorMap tcm = a.tma_epi ? *static_cast<const CUtensorMap*>(tmap_c) : tw;
-  const ConvKernel kern = trace ? pick_conv<true>(a.mode, a.tma_epi != 0) : pick_conv<false>(a.mode, a.tma_epi != 0);
+  const ConvKernel kern = pick_conv(a.mode, a.tma_epi != 0, trace != nullptr, g.x3);
+  if (!kern) return false;
   if (cudaLaunchKernelEx(&cfg, kern, tx, tw, tcm, a) != cudaSuccess) {
     cudaGetLastError();
     return false;

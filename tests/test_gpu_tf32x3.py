@@ -70,3 +70,39 @@ def test_3xtf32_fp32_accuracy_on_normal_inputs():
     assert err["tcgen05"] < 1e-5, err
     assert err["tcgen05"] < 8 * err["simt"] + 1e-7, err
     r.close()
+
+
+def test_3xtf32_conv_configurations_exact_and_fp32_accurate():
+    # fp32 conv2d: every tcgen05_conv configuration (cfg[7] = 1: 3xTF32
+    # halves of the input activation and the K-major weights) bit-exact after
+    # 8 chained launches on integer inputs, and within fp32 tolerance on N(0,1)
+    hdr, pop = load_population("conv2d")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    r = make_runner(min_repeats=8, max_repeats=8, timeout_ms=50.0)
+    r.set_workload(e0, seed=2)
+    want = next(iter(O.reference_outputs(e0, random_inputs(e0, 2)).values()))
+    plans = r.plan_programs(progs)
+    seen = {}
+    for i, p in enumerate(plans):
+        if p["family"] == "tcgen05_conv" and p["status"] == "OK":
+            assert p["cfg"][7] == 1, p
+            seen.setdefault(tuple(p["cfg"]), i)
+    assert len(seen) >= 4, len(seen)
+    for cfg, i in seen.items():
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] == "OK" and res["mismatches"] == 0 and res["repeats"] == 8, (cfg, res)
+        assert np.array_equal(r.last_output().astype(np.float64), want), cfg
+    r.close()
+    ins = normal_inputs(e0, 7)
+    want = next(iter(O.reference_outputs(e0, {k: v.astype(np.float32) for k, v in ins.items()}).values()))
+    scale = np.abs(want).max()
+    r = make_runner(rtol=1e-4, atol=1e-4 * scale, timeout_ms=50.0)
+    r.set_workload(e0, inputs=ins)
+    for cfg, i in list(seen.items())[:4]:
+        res, = r.measure_programs([progs[i]])
+        assert res["status"] == "OK", (cfg, res)
+        out = r.last_output().astype(np.float64)
+        np.testing.assert_allclose(out, want, rtol=1e-4, atol=1e-4 * scale)
+        assert np.abs(out - want).max() / scale < 1e-5, cfg
+    r.close()
