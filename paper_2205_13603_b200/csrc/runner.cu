@@ -151,6 +151,7 @@ struct ls_runner {
   bool bf16 = false;
   bool have_workload = false;
   bool best_valid = false;  // device best-so-far initialised for this workload (carry_best)
+  int64_t setup_launches = 0;  // kernels of the last set_workload, reported by the next measure call's count
   Workload w;
   std::string e0_text;
   bool tc_ok = false;
@@ -237,6 +238,7 @@ struct ls_runner {
     tmap_am.clear();
     have_tmap_c = false;
     have_workload = false;
+    setup_launches = 0;
   }
   void release() {
     cudaSetDevice(device);
@@ -590,6 +592,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
         LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&tmp), n * 4));
         LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[inp], n * 4, cudaMemcpyHostToDevice, r->st));
         launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(r->gbuf[b]), elems, r->st);
+        ++r->setup_launches;
         LSB_CUDA(cudaStreamSynchronize(r->st));
         r->pfree(tmp);
       } else {
@@ -633,7 +636,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     for (int d = 0; d < gen.ndim[b]; ++d) B.shape[b][d] = gen.shape[b][d];
   }
   for (const GenBlock& g : gen.blocks)
-    if (!launch_generic_block(g, code, B, true, nullptr, nullptr, r->st)) {
+    if (++r->setup_launches, !launch_generic_block(g, code, B, true, nullptr, nullptr, r->st)) {
       set_error("reference run of e0 failed to launch");
       return LS_ERR_CUDA;
     }
@@ -655,6 +658,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
     if (r->wt_rows % 64 || r->wt_cols % 16) break;
     if (r->bf16) {
       LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 2));
+      ++r->setup_launches;
       launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->gbuf[b]), static_cast<__nv_bfloat16*>(r->wt), 1,
                             r->wt_rows, r->wt_cols, r->st);
       LSB_CUDA(cudaGetLastError());
@@ -663,6 +667,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
       // 3xTF32 conv tile: weight halves K-major, and halves of every NHWC
       // input whose channels fill whole 32-element (128-byte) rows
       LSB_CUDA(r->pmalloc(&r->wt, static_cast<size_t>(elems) * 8));
+      ++r->setup_launches;
       launch_split_tf32(static_cast<const float*>(r->gbuf[b]), static_cast<float*>(r->wt), 1, r->wt_rows, r->wt_cols,
                         true, r->st);
       r->gbuf_x3.assign(nb, nullptr);
@@ -671,6 +676,7 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
         int64_t xe = 1;
         for (int64_t v : gw.shapes[x]) xe *= v;
         LSB_CUDA(r->pmalloc(&r->gbuf_x3[x], static_cast<size_t>(xe) * 8));
+        ++r->setup_launches;
         launch_split_tf32(static_cast<const float*>(r->gbuf[x]), static_cast<float*>(r->gbuf_x3[x]), 1,
                           xe / gw.shapes[x][3], gw.shapes[x][3], false, r->st);
       }
@@ -874,6 +880,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
       LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&tmp), static_cast<size_t>(elems) * 4));
       LSB_CUDA(cudaMemcpyAsync(tmp, host_inputs[idx], static_cast<size_t>(elems) * 4, cudaMemcpyHostToDevice, r->st));
       launch_to_bf16(tmp, static_cast<__nv_bfloat16*>(*dst), elems, r->st);
+      ++r->setup_launches;
       LSB_CUDA(cudaStreamSynchronize(r->st));
       r->pfree(tmp);
     }
@@ -889,6 +896,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
   LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->c), static_cast<size_t>(w.c_elems) * 4));
   LSB_CUDA(r->pmalloc(reinterpret_cast<void**>(&r->ref), static_cast<size_t>(w.c_elems) * 8));
   launch_reference(r->x, r->y, r->ref, r->s, r->bf16, r->st);
+  ++r->setup_launches;
   LSB_CUDA(cudaGetLastError());
 
   // tcgen05 operands: X must be [batch][M][K]; Y is used K-major ([batch][N][K]),
@@ -904,6 +912,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
     LSB_CUDA(r->pmalloc(&r->xs, static_cast<size_t>(w.x_elems) * 8));
     LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 8));
     launch_split_tf32(static_cast<const float*>(r->x), static_cast<float*>(r->xs), B, M, K, false, r->st);
+    r->setup_launches += 2;
     if (y_kmaj) launch_split_tf32(static_cast<const float*>(r->y), static_cast<float*>(r->yk), B, N, K, false, r->st);
     else launch_split_tf32(static_cast<const float*>(r->y), static_cast<float*>(r->yk), B, K, N, true, r->st);
     LSB_CUDA(cudaGetLastError());
@@ -919,6 +928,7 @@ ls_status ls_runner_set_workload(ls_runner* r, const char* e0, size_t len, const
       LSB_CUDA(cudaMemcpyAsync(r->yk, r->y, static_cast<size_t>(w.y_elems) * 2, cudaMemcpyDeviceToDevice, r->st));
     } else {
       LSB_CUDA(r->pmalloc(&r->yk, static_cast<size_t>(w.y_elems) * 2));
+      ++r->setup_launches;
       launch_transpose_bf16(static_cast<const __nv_bfloat16*>(r->y), static_cast<__nv_bfloat16*>(r->yk), B, K, N,
                             r->st);
       LSB_CUDA(cudaGetLastError());
@@ -994,7 +1004,8 @@ ls_status ls_runner_measure(ls_runner* r, const char* const* programs, const siz
            r->has_alt ? &r->gw : nullptr);
   const double plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
   for (int i = 0; i < n; ++i) fill_result(plans[static_cast<size_t>(i)], &out[i]);
-  r->launches = 0;
+  r->launches = r->setup_launches;  // the preceding set_workload's kernels are counted once, here
+  r->setup_launches = 0;
   bool any_gp = false;
   for (const Plan& p : plans) any_gp |= p.gp != nullptr;
   if (any_gp) {  // one upload of every candidate's bytecode

@@ -483,3 +483,21 @@ def test_trace_tc_kernel_span():
     res, = r.measure_programs([progs[i]])
     assert res["status"] == "OK" and res["mismatches"] == 0
     r.close()
+
+
+def test_launch_count_includes_set_workload_kernels():
+    # the kernels set_workload enqueues (2 bf16 conversions, the fp64
+    # reference, the K-major transpose) are reported once, by the next
+    # measure call's launch count
+    hdr, pop = load_population("bert_ffn")
+    e0 = hdr["e0"]
+    progs = [p["program"] for p in pop]
+    r = make_runner("bf16", min_repeats=3, max_repeats=3)
+    r.set_workload(e0, seed=0)
+    i = next(i for i, p in enumerate(r.plan_programs(progs)) if p["family"] == "tcgen05" and p["status"] == "OK")
+    r.measure_programs([progs[i]])
+    first = r.launch_count()
+    r.measure_programs([progs[i]])
+    second = r.launch_count()
+    assert first - second == 4, (first, second)
+    r.close()
