@@ -648,10 +648,11 @@ GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const Devic
       }
     }
     // ---- TCGEN05 conv: innermost [p 8][q 8][co BN][ci 64] (bf16) ----
-    // fp32: the 3xTF32 tile reads operand halves the runner splits once, so
-    // its activation must be a workload input (not an in-candidate pad stage)
-    const bool x3_ok = lim.tf32x3 && p.buffers[static_cast<size_t>(xl->buffer)].role == 0;
-    if ((lim.bf16 || x3_ok) && tc_conv_plan(w, p, s, xl, yl, lps, cond != nullptr, lim, &step.conv)) {
+    // fp32: the 3xTF32 tile reads operand halves; the runner splits a
+    // workload input once and an in-candidate activation (a pad stage's
+    // output) on every launch, right before the conv step
+    if ((lim.bf16 || lim.tf32x3) && tc_conv_plan(w, p, s, xl, yl, lps, cond != nullptr, lim, &step.conv)) {
+      step.x3_split = step.conv.x3 && p.buffers[static_cast<size_t>(xl->buffer)].role != 0;
       step.family = F_TCCONV;
       step.x_buf = xl->buffer;
       step.y_buf = yl->buffer;

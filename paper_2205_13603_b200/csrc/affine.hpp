@@ -91,6 +91,7 @@ struct GStep {
   TcConvCfg conv{};
   CopyCfg copy{};
   int x_buf = -1, y_buf = -1, c_buf = -1;  // candidate buffer ids (SIMT-A, TC-conv)
+  bool x3_split = false;    // 3xTF32 conv on an in-candidate activation: split it into halves each launch
 };
 
 struct GeneralPlan {
@@ -102,6 +103,13 @@ struct GeneralPlan {
   int32_t cfg[13] = {0};
   int family = 0;           // family of the contraction step (reporting)
 };
+
+// kernels one launch of a general plan enqueues (a step, plus its per-launch split)
+inline int64_t general_kernels(const GeneralPlan& g) {
+  int64_t n = 0;
+  for (const GStep& s : g.steps) n += s.x3_split ? 2 : 1;
+  return n;
+}
 
 struct DeviceLimits;
 GeneralPlan plan_general(const GeneralWorkload& w, const Program& p, const DeviceLimits& lim);

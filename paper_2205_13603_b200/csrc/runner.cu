@@ -349,7 +349,7 @@ struct ls_runner {
   // tcgen05 conv: K-major weight copy [n_cols][k_rows] and tensor-map caches
   void* wt = nullptr;            // bf16; fp32 workloads: [hi | lo] halves (3xTF32)
   int64_t wt_rows = 0, wt_cols = 0;
-  std::vector<void*> gbuf_x3;    // fp32 workloads: [hi | lo] halves of each NHWC input (or null)
+  std::vector<void*> gbuf_x3;    // fp32 workloads: [hi | lo] halves of each NHWC buffer (or null)
   std::map<int, CUtensorMap> tmap_wt;         // by BN
   std::map<const void*, CUtensorMap> tmap_x;  // by activation buffer
 
@@ -408,6 +408,11 @@ struct ls_runner {
           const size_t gi = static_cast<size_t>(it - gw.buffers.begin());
           if (it == gw.buffers.end() || gi >= gbuf_x3.size() || !gbuf_x3[gi]) return false;
           xsrc = gbuf_x3[gi];
+          if (stp.x3_split) {  // the activation was written by an earlier step of this launch
+            const int64_t* sh = B.shape[stp.x_buf];
+            launch_split_tf32(static_cast<const float*>(B.ptr[stp.x_buf]), static_cast<float*>(gbuf_x3[gi]), 1,
+                              sh[0] * sh[1] * sh[2], sh[3], false, q);
+          }
         }
         const CUtensorMap* mx = map_x(xsrc, B.shape[stp.x_buf]);
         const CUtensorMap* mw = map_wt(static_cast<int>(stp.conv.bn));
@@ -449,7 +454,7 @@ struct ls_runner {
     const unsigned long long* dl = guarded ? deadline : nullptr;
     int* flag = flags + slot;
     if (p.gp) {
-      launches += static_cast<int64_t>(p.gp->steps.size());
+      launches += general_kernels(*p.gp);
       return launch_general(p, dl, flag, slot, q);
     }
     const size_t cbytes = static_cast<size_t>(w.c_elems) * sizeof(float);
@@ -503,7 +508,7 @@ struct ls_runner {
 namespace {
 
 // kernels one Runner::launch of a plan enqueues (as counted in launches)
-int64_t kernels_per_launch(const Plan& p) { return p.gp ? static_cast<int64_t>(p.gp->steps.size()) : 1; }
+int64_t kernels_per_launch(const Plan& p) { return p.gp ? general_kernels(*p.gp) : 1; }
 
 // alt: for contraction workloads, the general-path view of the same e0; a
 // candidate the contraction instantiator cannot map (e.g. a PVU schedule
@@ -671,11 +676,12 @@ ls_status set_general_workload(ls_runner* r, const Program& e0, const GeneralWor
       launch_split_tf32(static_cast<const float*>(r->gbuf[b]), static_cast<float*>(r->wt), 1, r->wt_rows, r->wt_cols,
                         true, r->st);
       r->gbuf_x3.assign(nb, nullptr);
-      for (size_t x = 0; x < nb; ++x) {
-        if (gw.roles[x] != 0 || gw.shapes[x].size() != 4 || gw.shapes[x][3] % 32) continue;
+      for (size_t x = 0; x < nb; ++x) {  // inputs split here; intermediates on every launch
+        if (gw.roles[x] == 1 || gw.shapes[x].size() != 4 || gw.shapes[x][3] % 32) continue;
         int64_t xe = 1;
         for (int64_t v : gw.shapes[x]) xe *= v;
         LSB_CUDA(r->pmalloc(&r->gbuf_x3[x], static_cast<size_t>(xe) * 8));
+        if (gw.roles[x] != 0) continue;
         ++r->setup_launches;
         launch_split_tf32(static_cast<const float*>(r->gbuf[x]), static_cast<float*>(r->gbuf_x3[x]), 1,
                           xe / gw.shapes[x][3], gw.shapes[x][3], false, r->st);
