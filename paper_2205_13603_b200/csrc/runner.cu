@@ -403,7 +403,7 @@ struct ls_runner {
       if (stp.family == F_TCCONV) {
         if (p.gp->gen.ndim[stp.x_buf] != 4 || B.dtype[stp.x_buf] != (stp.conv.x3 ? 1 : 0)) return false;
         const void* xsrc = B.ptr[stp.x_buf];
-        if (stp.conv.x3) {  // the activation's [hi | lo] halves (a workload input, split at set_workload)
+        if (stp.conv.x3) {  // the activation's [hi | lo] halves (an input's: split at set_workload)
           auto it = std::find(gw.buffers.begin(), gw.buffers.end(), p.gp->buf_names[static_cast<size_t>(stp.x_buf)]);
           const size_t gi = static_cast<size_t>(it - gw.buffers.begin());
           if (it == gw.buffers.end() || gi >= gbuf_x3.size() || !gbuf_x3[gi]) return false;
