@@ -40,6 +40,7 @@ WORKLOADS = {
     "gmm512": ("pop_gmm512.jsonl.gz", "f32", "GEMM 512x512x512 fp32"),
     "gmm512_tc": ("pop_gmm512_tc.jsonl.gz", "f32", "GEMM 512x512x512 fp32 with tcgen05 tensorize (3xTF32)"),
     "conv2d": ("pop_conv2d.jsonl.gz", "bf16", "ResNet-50 conv2d 56x56x64->64 3x3 NHWC bf16 implicit GEMM"),
+    "conv2d_f32": ("pop_conv2d.jsonl.gz", "f32", "ResNet-50 conv2d 56x56x64->64 3x3 NHWC fp32 implicit GEMM (3xTF32 tcgen05)"),
 }
 
 
@@ -410,7 +411,7 @@ def run_b200(args):
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
     # an fp32 tcgen05 tile runs as 3xTF32: three kind::tf32 passes at half the
     # bf16 rate, so its roof is bf16 / 6 in fp32 FLOP/s
-    x3 = dtype != "bf16" and best is not None and best["family"] == "tcgen05"
+    x3 = dtype != "bf16" and best is not None and best["family"] in ("tcgen05", "tcgen05_conv")
     peak = peak_bf16 if dtype == "bf16" else peak_bf16 / 6 if x3 else fp32_peak
     bound = "tensor" if dtype == "bf16" else "tensor (3xTF32)" if x3 else "fp32-simt"
     algo_bytes = algorithmic_bytes(e0, dtype)
