@@ -1,7 +1,7 @@
 """Per-launch latency of the fastest schedules of a family against the number
 of timed repeats in the runner's graph: a fixed per-graph cost (graph start,
 first-launch effects) shows up as latency falling with the repeat count.
-  python scripts/repeat_sweep.py bmm_qk tcgen05"""
+  python scripts/repeat_sweep.py bmm_qk tcgen05 [dtype]"""
 import os
 import sys
 
@@ -12,9 +12,10 @@ from conftest import load_population  # noqa: E402
 from paper_2205_13603_b200.runner import B200Runner  # noqa: E402
 
 workload, family = sys.argv[1], sys.argv[2]
+DT = sys.argv[3] if len(sys.argv) > 3 else ("f32" if workload.startswith("gmm512") else "bf16")
 hdr, pop = load_population(workload)
 progs = [p["program"] for p in pop]
-probe = B200Runner(dtype="bf16", min_repeats=50, max_repeats=2000, target_ms=0.5, timeout_ms=5.0)
+probe = B200Runner(dtype=DT, min_repeats=50, max_repeats=2000, target_ms=0.5, timeout_ms=5.0)
 probe.set_workload(hdr["e0"])
 plans = probe.plan_programs(progs)
 idx = [i for i, p in enumerate(plans) if p["family"] == family and p["status"] == "OK"]
@@ -31,7 +32,7 @@ for j in sorted(range(len(idx)), key=lambda j: res[j]["latency_ns"] if res[j]["s
 print("cfg | us/launch at min_repeats 50, 200, 800, 2000")
 rows = {i: [] for i in top}
 for reps in (50, 200, 800, 2000):
-    r = B200Runner(dtype="bf16", min_repeats=reps, max_repeats=reps, target_ms=0.0, timeout_ms=5.0)
+    r = B200Runner(dtype=DT, min_repeats=reps, max_repeats=reps, target_ms=0.0, timeout_ms=5.0)
     r.set_workload(hdr["e0"])
     out = r.measure_programs([progs[i] for i in top])
     r.close()
