@@ -120,3 +120,18 @@ def test_reference_record_files_still_load(tmp_path):
     ls.search.save_records(str(tmp_path / "ref.jsonl"), rep.log)
     got = R.load_records(str(tmp_path / "ref.jsonl"), unit="cycles")
     assert [g.latency for g in got] == [r.latency for r in rep.log]
+
+
+def test_roofline_bound_follows_the_best_family(tmp_path):
+    # tcgen05 best -> tensor bound; an fp32 SIMT best -> fp32-simt bound
+    _, doc = run(tmp_path)
+    assert doc["hardware"]["best"]["roofline"]["bound"] == "tensor"
+    from paper_2205_13603_b200.records import HardwareContext, report_json
+    report, _ = run(tmp_path, out="rec2.jsonl")
+    from paper_2205_13603_b200.refapi import loopsched
+    ctx = HardwareContext.for_workload(loopsched().gmm(64, 64, 64), dtype="f32", peak_tflops=74.4,
+                                       peak_source="fp32 SIMT nominal")
+    simt = report_json(report, ctx, info={report.best.program_hash: {"family": "simt"}})
+    assert simt["hardware"]["best"]["roofline"]["bound"] == "fp32-simt"
+    x3 = report_json(report, ctx, info={report.best.program_hash: {"family": "tcgen05"}})
+    assert x3["hardware"]["best"]["roofline"]["bound"] == "tensor"
