@@ -15,10 +15,11 @@ ap.add_argument("--family", default="tcgen05")
 ap.add_argument("--count", type=int, default=8)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cfg", default="")
+ap.add_argument("--dtype", default="")
 ap.add_argument("--host-us", type=float, default=0.0)  # comma list of cfg prefixes to select, e.g. "1,1,12,64,12"
 args = ap.parse_args()
 hdr, pop = load_population(args.workload)
-dtype = "f32" if args.workload.startswith("gmm512") else "bf16"
+dtype = args.dtype or ("f32" if args.workload.startswith("gmm512") else "bf16")
 r = B200Runner(dtype=dtype, min_repeats=args.reps, max_repeats=args.reps, target_ms=0.001, timeout_ms=5)
 r.set_workload(hdr["e0"])
 progs = [p["program"] for p in pop]
